@@ -1,0 +1,160 @@
+"""Execution states, convex subgraphs and candidate kernels (test infrastructure only).
+
+Definitions:
+  convex subgraph   no p1, p2 in P', q not in P' with p1 ~> q ~> p2
+  execution state   for every edge (p1,p2): p2 in P' => p1 in P'
+  Theorem 1         convex <=> difference of two execution states
+Candidate kernels follow readings A3/A4: a candidate is a convex
+set P' with a unique sink o (o has no successor inside P'); o is its single
+output ("each candidate kernel ... produces one output tensor").
+Pruning: more than max_prims primitives, or >= 2 dense linear
+primitives (reading A18), is rejected before profiling.
+
+This module deliberately does NOT run Alg. 1's DFS: states are enumerated by
+their definition (include/exclude in topological order), convexity by
+reachability.  The library's Alg. 1 output is compared against these.
+"""
+from __future__ import annotations
+
+from itertools import combinations
+
+from .operators import kahn_order
+from .primitives import is_dense_linear
+
+
+class PGraph:
+    """Node-only view of a primitive graph: preds/succs over primitive ids."""
+
+    def __init__(self, pg: dict):
+        self.pg = pg
+        self.n = len(pg["nodes"])
+        self.preds = [sorted({r[1] for r in nd["inputs"] if r[0] == "node"}) for nd in pg["nodes"]]
+        self.succs = [[] for _ in range(self.n)]
+        for v, ps in enumerate(self.preds):
+            for u in ps:
+                self.succs[u].append(v)
+        self.outputs = set(pg["outputs"])
+        self.topo = kahn_order([{"id": i} for i in range(self.n)], lambda nd: self.preds[nd["id"]])
+        self.topo_index = {v: i for i, v in enumerate(self.topo)}
+        self._reach = None
+
+    @classmethod
+    def from_edges(cls, n, edges, outputs=None):
+        nodes = [{"id": i, "kind": "relu", "attrs": {}, "inputs": [], "shape": (1,)} for i in range(n)]
+        for u, v in edges:
+            nodes[v]["inputs"].append(("node", u))
+        if outputs is None:
+            outputs = [i for i in range(n) if not any(u == i for u, _ in edges)]
+        return cls({"nodes": nodes, "outputs": outputs, "inputs": []})
+
+    def reach(self):
+        """reach[u] = set of nodes v with a non-empty path u ~> v."""
+        if self._reach is None:
+            r = [set() for _ in range(self.n)]
+            for u in reversed(self.topo):
+                for v in self.succs[u]:
+                    r[u].add(v)
+                    r[u] |= r[v]
+            self._reach = r
+        return self._reach
+
+
+def is_execution_state(g: PGraph, s) -> bool:
+    return all(p in s for v in s for p in g.preds[v])
+
+
+def is_convex(g: PGraph, s) -> bool:
+    """Definition, checked directly by reachability."""
+    s = set(s)
+    reach = g.reach()
+    outside = [q for q in range(g.n) if q not in s]
+    for q in outside:
+        if any(q in reach[p1] for p1 in s) and any(p2 in reach[q] for p2 in s):
+            return False
+    return True
+
+
+def execution_states(g: PGraph, cap: int = 1_000_000):
+    """All predecessor-closed subsets, INCLUDING the empty state (reading A1).
+
+    Enumerated by deciding include/exclude for nodes in topological order: a node may be
+    included only if all its predecessors are included.
+    """
+    topo = g.topo
+    out = []
+
+    def rec(i, cur):
+        if len(out) > cap:
+            raise RuntimeError("state explosion")
+        if i == len(topo):
+            out.append(frozenset(cur))
+            return
+        v = topo[i]
+        rec(i + 1, cur)                       # exclude v
+        if all(p in cur for p in g.preds[v]):  # include v
+            cur.add(v)
+            rec(i + 1, cur)
+            cur.remove(v)
+
+    rec(0, set())
+    return out
+
+
+def convex_sets_from_states(states):
+    """Theorem 1: { D2 \\ D1 : D1 subset D2 }, non-empty, deduplicated."""
+    res = set()
+    for d1 in states:
+        for d2 in states:
+            if d1 < d2:
+                res.add(d2 - d1)
+    return res
+
+
+def convex_sets_brute_force(g: PGraph):
+    """All non-empty subsets checked against the convexity definition (small graphs)."""
+    res = set()
+    for k in range(1, g.n + 1):
+        for c in combinations(range(g.n), k):
+            if is_convex(g, c):
+                res.add(frozenset(c))
+    return res
+
+
+def sinks(g: PGraph, s):
+    return [v for v in s if not any(w in s for w in g.succs[v])]
+
+
+def candidates(g: PGraph, convex_sets, max_prims=16, prune_linear=True):
+    """Unique-sink candidates (A4) after the P:626 pruning, in canonical order.
+
+    Canonical order: sort by (output id, popcount, member-id tuple).
+    Returns a list of (members: tuple sorted, output: int).
+    """
+    pg = g.pg
+    dense = set()
+    if prune_linear and "inputs" in pg:
+        shapes = {s["name"]: tuple(s["shape"]) for s in pg["inputs"]}
+        for nd in pg["nodes"]:
+            if nd["kind"] in ("matmul", "conv2d"):
+                ins = [shapes[r[1]] if r[0] == "input" else pg["nodes"][r[1]]["shape"]
+                       for r in nd["inputs"]]
+                if is_dense_linear(nd, ins):
+                    dense.add(nd["id"])
+    out = []
+    for s in convex_sets:
+        sk = sinks(g, s)
+        if len(sk) != 1:
+            continue
+        if len(s) > max_prims:
+            continue
+        if prune_linear and len(dense & s) >= 2:
+            continue
+        out.append((tuple(sorted(s)), sk[0]))
+    out.sort(key=lambda c: (c[1], len(c[0]), c[0]))
+    return out
+
+
+def candidate_inputs(g: PGraph, members):
+    """Primitive inputs of a candidate: nodes outside P' feeding P' (the I matrix row)."""
+    m = set(members)
+    return sorted({p for v in m for p in g.preds[v] if p not in m})
