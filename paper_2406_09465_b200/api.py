@@ -1,0 +1,205 @@
+"""Python front end of the C ABI (argument marshalling + the host-side BLP).
+
+    ctx = Context(0)
+    kg  = KorchGraph(ctx, graph_dict)          # korch_graph_load (fission inside)
+    kg.enumerate()                              # Alg. 1 + templates
+    costs = kg.profile()                        # on-device PROFILING, ns
+    sel = kg.select(costs)                      # Eq. 2-4 BLP (HiGHS)
+    kg.set_orchestration(sel)                   # Eq. 3/4 check, buffer plan
+    kg.execute(inputs, outputs, workspace, stream)   # CUDA-graph replay
+
+Device buffers are torch tensors (PyTorch is used for memory, streams and
+process groups only).
+"""
+from __future__ import annotations
+
+import ctypes as C
+import json
+import os
+
+from . import _lib
+from ._lib import LIB, check
+from .select import INF, operator_aligned, singletons, solve_blp
+
+DTYPE_BYTES = {"f32": 4, "bf16": 2}
+
+
+class Context:
+    def __init__(self, device: int = 0):
+        self.h = C.c_void_p()
+        check(LIB.korch_create(int(device), C.byref(self.h)))
+        self.device = device
+
+    def close(self):
+        if self.h:
+            LIB.korch_destroy(self.h)
+            self.h = C.c_void_p()
+
+    def __del__(self):  # pragma: no cover
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+class KorchGraph:
+    def __init__(self, ctx: Context, graph):
+        self.ctx = ctx
+        text = graph if isinstance(graph, str) else json.dumps(graph)
+        b = text.encode()
+        self.h = C.c_void_p()
+        check(LIB.korch_graph_load(ctx.h, b, len(b), C.byref(self.h)))
+        self.cands = None
+        self.n_states = None
+        self.prim = self.dump()
+        self.inputs = self.prim["inputs"]
+        self.outputs = self.prim["outputs"]
+        self.workspace_bytes = None
+
+    def __del__(self):  # pragma: no cover
+        try:
+            if self.h:
+                LIB.korch_graph_free(self.h)
+        except Exception:
+            pass
+
+    # ---------------------------------------------------------------- graph
+    def dump(self) -> dict:
+        need = C.c_size_t()
+        LIB.korch_graph_dump(self.h, None, 0, C.byref(need))
+        buf = C.create_string_buffer(need.value)
+        check(LIB.korch_graph_dump(self.h, buf, need.value, C.byref(need)))
+        return json.loads(buf.value.decode())
+
+    def validate(self) -> str:
+        buf = C.create_string_buffer(1 << 16)
+        check(LIB.korch_validate(self.h, buf, len(buf)))
+        return buf.value.decode()
+
+    @property
+    def n_prims(self):
+        return len(self.prim["nodes"])
+
+    def output_shape(self, k=0):
+        return tuple(self.prim["nodes"][self.outputs[k]]["shape"])
+
+    # ---------------------------------------------------------------- candidates
+    def enumerate(self, max_prims: int = 16, keep_multi_linear: bool = False, max_states: int = 1_000_000):
+        o = _lib.EnumOpts(max_prims, int(keep_multi_linear), max_states)
+        nc, ns = C.c_int64(), C.c_int64()
+        check(LIB.korch_enumerate(self.h, C.byref(o), C.byref(nc), C.byref(ns)))
+        self.n_states = ns.value
+        self.cands = [self.candidate(i) for i in range(nc.value)]
+        return self.cands
+
+    def candidate(self, i: int) -> dict:
+        d = _lib.CandDesc()
+        check(LIB.korch_candidate(self.h, i, C.byref(d)))
+        return {
+            "index": i,
+            "members": [d.members[k] for k in range(d.n_members)],
+            "output": d.output,
+            "inputs": [d.inputs[k] for k in range(d.n_inputs)],
+            "graph_inputs": [d.graph_inputs[k] for k in range(d.n_graph_inputs)],
+            "klass": _lib.CLASS_NAMES[d.klass],
+            "n_dense_linear": d.n_dense_linear,
+            "bytes": d.bytes,
+            "flops": d.flops,
+            "signature": d.signature.decode(),
+        }
+
+    def source(self, i: int) -> str:
+        need = C.c_size_t()
+        LIB.korch_candidate_source(self.h, i, None, 0, C.byref(need))
+        buf = C.create_string_buffer(max(1, need.value))
+        check(LIB.korch_candidate_source(self.h, i, buf, len(buf), C.byref(need)))
+        return buf.value.decode()
+
+    def generable(self):
+        return [c["index"] for c in self.cands if c["klass"] != "rejected"]
+
+    # ---------------------------------------------------------------- compile / profile
+    def compile(self, idx=None, threads: int = 0, cache_dir: str | None = None):
+        idx = self.generable() if idx is None else list(idx)
+        arr = _lib.i64_array(idx)
+        ok = (C.c_int32 * max(1, len(idx)))()
+        cd = cache_dir.encode() if cache_dir else None
+        check(LIB.korch_compile(self.h, arr, len(idx), threads, cd, ok))
+        return [ok[k] for k in range(len(idx))]
+
+    def profile(self, idx=None, warmup=3, launches=20, trials=5, flush_l2=False, tune=True,
+                compile_threads=0):
+        """PROFILING: median per-launch ns per candidate; INF if not generable."""
+        allidx = list(range(len(self.cands))) if idx is None else list(idx)
+        arr = _lib.i64_array(allidx)
+        out = (C.c_int64 * max(1, len(allidx)))()
+        o = _lib.ProfOpts(warmup, launches, trials, int(flush_l2), compile_threads, 0 if tune else -1)
+        check(LIB.korch_profile(self.h, arr, len(allidx), C.byref(o), out))
+        costs = [out[k] for k in range(len(allidx))]
+        if idx is None:
+            self.costs = costs
+        return costs
+
+    # ---------------------------------------------------------------- orchestration
+    def select(self, costs=None, time_limit=600.0):
+        costs = self.costs if costs is None else costs
+        return solve_blp(self.cands, costs, self.outputs, time_limit=time_limit)
+
+    def operator_aligned(self):
+        return operator_aligned(self.cands, self.prim)
+
+    def singletons(self):
+        return singletons(self.cands, self.n_prims)
+
+    def set_orchestration(self, sel) -> int:
+        arr = _lib.i64_array(list(sel))
+        ws = C.c_size_t()
+        check(LIB.korch_set_orchestration(self.h, arr, len(sel), C.byref(ws)))
+        self.workspace_bytes = ws.value
+        return ws.value
+
+    def plan(self):
+        n = C.c_int64()
+        check(LIB.korch_plan(self.h, C.byref(n), None))
+        arr = (C.c_int64 * max(1, n.value))()
+        check(LIB.korch_plan(self.h, C.byref(n), arr))
+        return [arr[k] for k in range(n.value)]
+
+    # ---------------------------------------------------------------- execution
+    def execute(self, inputs, outputs, workspace, stream=None):
+        """inputs/outputs: sequences of device pointers (int) or torch tensors."""
+        def ptr(t):
+            return t if isinstance(t, int) else t.data_ptr()
+        n_in, n_out = len(self.inputs), len(self.outputs)
+        if len(inputs) != n_in or len(outputs) != n_out:
+            raise ValueError("wrong number of inputs/outputs")
+        ia = (C.c_void_p * max(1, n_in))(*[ptr(t) for t in inputs])
+        oa = (C.c_void_p * max(1, n_out))(*[ptr(t) for t in outputs])
+        ws = ptr(workspace) if workspace is not None else 0
+        s = stream if isinstance(stream, int) or stream is None else stream.cuda_stream
+        check(LIB.korch_execute(self.h, ia, oa, C.c_void_p(ws), C.c_void_p(s or 0)))
+
+    # helpers for torch-resident buffers
+    def torch_outputs(self, device="cuda"):
+        import torch
+        dt = {"f32": torch.float32, "bf16": torch.bfloat16}[self.prim["dtype"]]
+        return [torch.empty(self.prim["nodes"][o]["shape"], dtype=dt, device=device) for o in self.outputs]
+
+    def torch_workspace(self, device="cuda"):
+        import torch
+        return torch.empty(max(256, self.workspace_bytes or 0), dtype=torch.uint8, device=device)
+
+
+def torch_inputs(graph: dict, arrays: dict, device="cuda"):
+    """Move seeded storage arrays (float32 or uint16 bf16 bits) to the device, in graph order."""
+    import numpy as np
+    import torch
+    out = []
+    for spec in graph["inputs"]:
+        a = arrays[spec["name"]]
+        if spec["dtype"] == "bf16":
+            t = torch.from_numpy(np.ascontiguousarray(a).view(np.int16)).view(torch.bfloat16)
+        else:
+            t = torch.from_numpy(np.ascontiguousarray(a, dtype=np.float32))
+        out.append(t.to(device))
+    return out

@@ -1,0 +1,53 @@
+// Kernel generation for candidate kernels: PROFILING's "generate a kernel for the
+// defined tensor algebra computation" half, re-designed for
+// sm_100a.  Each candidate maps to one template (SURVEY.md §8(a')); a template
+// specialises to CUDA source (all shapes/strides compile-time constants) that
+// NVRTC compiles for sm_100a.  Several launch variants per candidate play the
+// role of the paper's schedule tuning; the profiler keeps the fastest.
+#pragma once
+#include <string>
+#include <vector>
+
+#include "enumerate.h"
+#include "ir.h"
+
+namespace korch {
+
+struct TmaDesc {            // a 2-5D TMA tensor map the host encodes per launch
+  int tensor = -1;          // index into KernelPlan::ext (or -2 = output)
+  int rank = 0;
+  int64_t dims[5] = {0};    // elements, innermost first
+  int64_t strides[5] = {0}; // bytes, for dims 1..rank-1 (innermost stride is 1 element)
+  int64_t elem_off = 0;     // element offset of the view into the tensor
+  uint32_t box[5] = {0};
+  int dtype = 1;            // 0 = f32, 1 = bf16
+  int swizzle = 3;          // CU_TENSOR_MAP_SWIZZLE_128B
+};
+
+struct KernelVariant {
+  std::string name;
+  std::string source;
+  int block = 256;
+  int64_t grid = 1;
+  int smem = 0;             // dynamic shared memory bytes
+  int cluster = 1;
+  std::string tag;
+  std::vector<TmaDesc> tma; // passed (in order) after the pointer params
+};
+
+struct KernelPlan {
+  int klass = 0;            // KORCH_CLASS_*
+  std::string reject;       // reason if rejected
+  std::vector<Ref> ext;     // external tensors, in kernel-parameter order
+  std::vector<KernelVariant> variants;
+  int64_t bytes = 0;
+  double flops = 0;
+};
+
+KernelPlan generate_kernel(const Graph& g, const Candidate& c);
+KernelPlan generate_gemm(const Graph& g, const Candidate& c);   // gemm_gen.cpp
+std::string kernel_prelude();
+std::string fmt_float(double v);
+uint64_t fnv1a(const std::string& s);
+
+}  // namespace korch

@@ -1,0 +1,768 @@
+// C ABI (include/korch.h): graph load, enumeration, kernel generation/compilation,
+// on-device profiling (PROFILING) and the executor.
+#include <algorithm>
+#include <atomic>
+#include <chrono>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <fstream>
+#include <map>
+#include <memory>
+#include <mutex>
+#include <sstream>
+#include <thread>
+#include <unordered_map>
+
+#include "../../include/korch.h"
+#include "codegen.h"
+#include "cuda_api.h"
+#include "enumerate.h"
+#include "ir.h"
+
+using namespace korch;
+
+static thread_local std::string g_err = "no error";
+
+static korch_status fail(korch_status code, const std::string& msg) {
+  g_err = msg;
+  return code;
+}
+
+#define KORCH_TRY(...)                                             \
+  try {                                                            \
+    __VA_ARGS__                                                    \
+  } catch (KorchError & e) {                                       \
+    return fail(e.code, e.what());                                 \
+  } catch (std::exception & e) {                                   \
+    return fail(KORCH_E_ARG, std::string("internal: ") + e.what()); \
+  }
+
+#define CU_CHECK(expr)                                                        \
+  do {                                                                        \
+    CUresult _r = (expr);                                                     \
+    if (_r != CUDA_SUCCESS) throw KorchError(KORCH_E_CUDA, std::string(#expr) + ": " + cu_err(_r)); \
+  } while (0)
+
+// ------------------------------------------------------------------ compiled kernels
+struct Module {
+  std::string cubin;
+  std::string log;
+  bool compiled = false, failed = false;
+  CUmodule mod = nullptr;
+  CUfunction fn = nullptr;
+  std::mutex mu;
+};
+
+struct korch_ctx {
+  int device = -1;
+  bool gpu = false;
+  CUdevice dev = 0;
+  CUcontext cuctx = nullptr;
+  int sm_count = 0;
+  int l2_bytes = 0;
+  CUstream pstream = nullptr;           // profiling / capture stream
+  CUdeviceptr arena = 0;
+  size_t arena_bytes = 0;
+  CUdeviceptr flush = 0;
+  size_t flush_bytes = 0;
+  std::mutex mu;
+  std::map<std::string, std::unique_ptr<Module>> modules;  // kernel name -> module
+
+  void bind() {
+    if (!gpu) throw KorchError(KORCH_E_CUDA, "host-only context (created with device -1)");
+    CU_CHECK(cuda().cuCtxSetCurrent(cuctx));
+  }
+  Module* module_for(const std::string& name) {
+    std::lock_guard<std::mutex> lk(mu);
+    auto& m = modules[name];
+    if (!m) m.reset(new Module());
+    return m.get();
+  }
+  CUdeviceptr arena_get(size_t bytes) {
+    if (bytes > arena_bytes) {
+      if (arena) cuda().cuMemFree(arena);
+      arena = 0;
+      size_t b = std::max(bytes, (size_t)64 << 20);
+      CUresult r = cuda().cuMemAlloc(&arena, b);
+      if (r != CUDA_SUCCESS) throw KorchError(KORCH_E_OOM, "profiling arena: " + cu_err(r));
+      arena_bytes = b;
+    }
+    return arena;
+  }
+};
+
+struct CandState {
+  bool planned = false;
+  KernelPlan plan;
+  int best = -1;          // chosen variant
+  int64_t cost_ns = -1;
+  std::string sig;
+};
+
+struct BufRef {           // where a kernel argument lives at execute time
+  enum { Input, Output, Work } kind = Input;
+  int index = 0;          // input index / output index
+  size_t offset = 0;      // workspace offset
+};
+
+struct Step {
+  int cand = -1;
+  int variant = 0;
+  std::vector<BufRef> args;
+  BufRef out;
+};
+
+struct korch_graph {
+  korch_ctx* ctx = nullptr;
+  Graph g;
+  bool enumerated = false;
+  std::vector<Candidate> cands;
+  std::vector<CandState> cs;
+  int64_t n_states = 0;
+  // accepted orchestration
+  bool has_plan = false;
+  std::vector<Step> steps;
+  size_t ws_bytes = 0;
+  // captured executable
+  std::vector<const void*> cap_ptrs;
+  CUgraphExec gexec = nullptr;
+  std::mutex mu;
+  ~korch_graph() {
+    if (gexec && cuda().ok) cuda().cuGraphExecDestroy(gexec);
+  }
+};
+
+// ------------------------------------------------------------------ generation
+static void ensure_planned(korch_graph* G, int64_t i) {
+  CandState& s = G->cs[i];
+  if (s.planned) return;
+  s.plan = generate_kernel(G->g, G->cands[i]);
+  Candidate& c = G->cands[i];
+  c.klass = s.plan.klass;
+  c.reject_reason = s.plan.reject;
+  if (s.plan.klass != KORCH_CLASS_REJECTED) {
+    c.bytes = s.plan.bytes;
+    c.flops = s.plan.flops;
+    c.signature = s.plan.variants[0].name;
+  } else {
+    c.signature = "rejected: " + s.plan.reject;
+  }
+  s.planned = true;
+}
+
+static std::string full_source(const KernelVariant& v) { return kernel_prelude() + v.source; }
+
+static bool compile_module(Module* m, const KernelVariant& v, const std::string& cache_dir) {
+  std::lock_guard<std::mutex> lk(m->mu);
+  if (m->compiled) return true;
+  if (m->failed) return false;
+  std::string path;
+  if (!cache_dir.empty()) {
+    path = cache_dir + "/" + v.name + ".cubin";
+    std::ifstream f(path, std::ios::binary);
+    if (f) {
+      std::stringstream ss;
+      ss << f.rdbuf();
+      m->cubin = ss.str();
+      if (!m->cubin.empty()) {
+        m->compiled = true;
+        return true;
+      }
+    }
+  }
+  NvrtcApi& nv = nvrtc();
+  if (!nv.ok) {
+    m->failed = true;
+    m->log = nv.err;
+    return false;
+  }
+  std::string src = full_source(v);
+  nvrtcProgram prog;
+  if (nv.nvrtcCreateProgram(&prog, src.c_str(), (v.name + ".cu").c_str(), 0, nullptr, nullptr) != NVRTC_SUCCESS) {
+    m->failed = true;
+    m->log = "nvrtcCreateProgram failed";
+    return false;
+  }
+  const char* opts[] = {"-arch=sm_100a", "-std=c++17", "-default-device", "-lineinfo", "-DNDEBUG", "--diag-suppress=177,550"};
+  nvrtcResult r = nv.nvrtcCompileProgram(prog, 6, opts);
+  size_t ls = 0;
+  nv.nvrtcGetProgramLogSize(prog, &ls);
+  std::string log(ls, '\0');
+  if (ls) nv.nvrtcGetProgramLog(prog, &log[0]);
+  if (r != NVRTC_SUCCESS) {
+    m->failed = true;
+    m->log = std::string("NVRTC: ") + nv.nvrtcGetErrorString(r) + "\n" + log;
+    nv.nvrtcDestroyProgram(&prog);
+    return false;
+  }
+  size_t cs = 0;
+  nv.nvrtcGetCUBINSize(prog, &cs);
+  m->cubin.resize(cs);
+  nv.nvrtcGetCUBIN(prog, &m->cubin[0]);
+  nv.nvrtcDestroyProgram(&prog);
+  m->compiled = true;
+  if (!path.empty()) {
+    std::string tmp = path + ".tmp" + std::to_string((uintptr_t)m);
+    std::ofstream f(tmp, std::ios::binary);
+    f.write(m->cubin.data(), (std::streamsize)m->cubin.size());
+    f.close();
+    std::rename(tmp.c_str(), path.c_str());
+  }
+  return true;
+}
+
+static void compile_many(korch_graph* G, const std::vector<int64_t>& idx, int threads, const std::string& cache_dir) {
+  std::vector<std::pair<Module*, const KernelVariant*>> jobs;
+  std::map<Module*, bool> seen;
+  for (int64_t i : idx) {
+    ensure_planned(G, i);
+    CandState& s = G->cs[i];
+    if (s.plan.klass == KORCH_CLASS_REJECTED) continue;
+    for (auto& v : s.plan.variants) {
+      Module* m = G->ctx->module_for(v.name);
+      if (m->compiled || m->failed || seen.count(m)) continue;
+      seen[m] = true;
+      jobs.push_back({m, &v});
+    }
+  }
+  if (threads <= 0) threads = (int)std::max(1u, std::thread::hardware_concurrency());
+  threads = std::min<int>(threads, (int)std::max<size_t>(1, jobs.size()));
+  std::atomic<size_t> next{0};
+  auto worker = [&] {
+    for (;;) {
+      size_t k = next++;
+      if (k >= jobs.size()) break;
+      compile_module(jobs[k].first, *jobs[k].second, cache_dir);
+    }
+  };
+  std::vector<std::thread> ts;
+  for (int t = 1; t < threads; ++t) ts.emplace_back(worker);
+  worker();
+  for (auto& t : ts) t.join();
+}
+
+static std::string default_cache_dir() {
+  const char* e = getenv("KORCH_CACHE_DIR");
+  return e ? e : "";
+}
+
+static CUfunction load_fn(korch_ctx* ctx, Module* m, const KernelVariant& v) {
+  std::lock_guard<std::mutex> lk(m->mu);
+  if (m->fn) return m->fn;
+  if (!m->compiled) throw KorchError(KORCH_E_NVRTC, "kernel not compiled: " + m->log);
+  CU_CHECK(cuda().cuModuleLoadData(&m->mod, m->cubin.data()));
+  CU_CHECK(cuda().cuModuleGetFunction(&m->fn, m->mod, v.name.c_str()));
+  if (v.smem > 48 * 1024)
+    CU_CHECK(cuda().cuFuncSetAttribute(m->fn, CU_FUNC_ATTRIBUTE_MAX_DYNAMIC_SHARED_SIZE_BYTES, v.smem));
+  (void)ctx;
+  return m->fn;
+}
+
+// ------------------------------------------------------------------ launching
+static void encode_tma(const TmaDesc& d, const void* base, CUtensorMap* out) {
+  cuuint64_t dims[5], strides[4];
+  cuuint32_t box[5], es[5];
+  int esz = d.dtype == 0 ? 4 : 2;
+  for (int i = 0; i < d.rank; ++i) {
+    dims[i] = (cuuint64_t)d.dims[i];
+    box[i] = d.box[i];
+    es[i] = 1;
+    if (i > 0) strides[i - 1] = (cuuint64_t)d.strides[i];
+  }
+  const char* p = static_cast<const char*>(base) + d.elem_off * esz;
+  CU_CHECK(cuda().cuTensorMapEncodeTiled(
+      out, d.dtype == 0 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT32 : CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, (cuuint32_t)d.rank,
+      const_cast<char*>(p), dims, strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
+      (CUtensorMapSwizzle)d.swizzle, CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE));
+}
+
+static void launch_variant(korch_ctx* ctx, const KernelPlan& plan, int vi, const std::vector<const void*>& ins,
+                           void* out, CUstream stream) {
+  const KernelVariant& v = plan.variants[vi];
+  Module* m = ctx->module_for(v.name);
+  CUfunction fn = load_fn(ctx, m, v);
+  std::vector<CUdeviceptr> ptrs(ins.size() + 1);
+  std::vector<void*> args;
+  args.reserve(ins.size() + 1 + v.tma.size());
+  for (size_t i = 0; i < ins.size(); ++i) {
+    ptrs[i] = (CUdeviceptr)ins[i];
+    args.push_back(&ptrs[i]);
+  }
+  ptrs[ins.size()] = (CUdeviceptr)out;
+  args.push_back(&ptrs[ins.size()]);
+  std::vector<CUtensorMap> maps(v.tma.size());
+  for (size_t t = 0; t < v.tma.size(); ++t) {
+    const TmaDesc& d = v.tma[t];
+    const void* base = d.tensor == -2 ? out : ins.at(d.tensor);
+    encode_tma(d, base, &maps[t]);
+    args.push_back(&maps[t]);
+  }
+  if (v.cluster > 1) {
+    CUlaunchConfig cfg{};
+    cfg.gridDimX = (unsigned)v.grid;
+    cfg.gridDimY = cfg.gridDimZ = 1;
+    cfg.blockDimX = (unsigned)v.block;
+    cfg.blockDimY = cfg.blockDimZ = 1;
+    cfg.sharedMemBytes = (unsigned)v.smem;
+    cfg.hStream = stream;
+    CUlaunchAttribute at;
+    at.id = CU_LAUNCH_ATTRIBUTE_CLUSTER_DIMENSION;
+    at.value.clusterDim.x = (unsigned)v.cluster;
+    at.value.clusterDim.y = at.value.clusterDim.z = 1;
+    cfg.attrs = &at;
+    cfg.numAttrs = 1;
+    CU_CHECK(cuda().cuLaunchKernelEx(&cfg, fn, args.data(), nullptr));
+  } else {
+    CU_CHECK(cuda().cuLaunchKernel(fn, (unsigned)v.grid, 1, 1, (unsigned)v.block, 1, 1, (unsigned)v.smem, stream,
+                                   args.data(), nullptr));
+  }
+}
+
+static int64_t tensor_bytes(const Graph& g, const Ref& r) { return numel(g.shape_of(r)) * dtype_size(g.dtype_of(r)); }
+
+// ------------------------------------------------------------------ API
+extern "C" {
+
+const char* korch_version(void) { return "korch-b200 0.1 (sm_100a)"; }
+const char* korch_last_error(void) { return g_err.c_str(); }
+
+korch_status korch_create(int32_t device, korch_ctx** out) {
+  if (!out) return fail(KORCH_E_ARG, "out is NULL");
+  KORCH_TRY({
+    std::unique_ptr<korch_ctx> c(new korch_ctx());
+    c->device = device;
+    if (device >= 0) {
+      CudaApi& cu = cuda();
+      if (!cu.ok) return fail(KORCH_E_CUDA, cu.err);
+      CU_CHECK(cu.cuDeviceGet(&c->dev, device));
+      CU_CHECK(cu.cuDevicePrimaryCtxRetain(&c->cuctx, c->dev));
+      CU_CHECK(cu.cuCtxSetCurrent(c->cuctx));
+      CU_CHECK(cu.cuDeviceGetAttribute(&c->sm_count, CU_DEVICE_ATTRIBUTE_MULTIPROCESSOR_COUNT, c->dev));
+      CU_CHECK(cu.cuDeviceGetAttribute(&c->l2_bytes, CU_DEVICE_ATTRIBUTE_L2_CACHE_SIZE, c->dev));
+      CU_CHECK(cu.cuStreamCreate(&c->pstream, CU_STREAM_NON_BLOCKING));
+      c->gpu = true;
+    }
+    *out = c.release();
+    return KORCH_OK;
+  })
+}
+
+korch_status korch_destroy(korch_ctx* c) {
+  if (!c) return KORCH_OK;
+  if (c->gpu && cuda().ok) {
+    cuda().cuCtxSetCurrent(c->cuctx);
+    cuda().cuCtxSynchronize();
+    for (auto& kv : c->modules)
+      if (kv.second->mod) cuda().cuModuleUnload(kv.second->mod);
+    if (c->arena) cuda().cuMemFree(c->arena);
+    if (c->flush) cuda().cuMemFree(c->flush);
+    if (c->pstream) cuda().cuStreamDestroy(c->pstream);
+    cuda().cuDevicePrimaryCtxRelease(c->dev);
+  }
+  delete c;
+  return KORCH_OK;
+}
+
+korch_status korch_graph_load(korch_ctx* ctx, const char* json, size_t n, korch_graph** out) {
+  if (!ctx || !json || !out) return fail(KORCH_E_ARG, "NULL argument");
+  KORCH_TRY({
+    std::unique_ptr<korch_graph> G(new korch_graph());
+    G->ctx = ctx;
+    G->g = load_graph(json, n);
+    *out = G.release();
+    return KORCH_OK;
+  })
+}
+
+korch_status korch_graph_free(korch_graph* g) {
+  if (g && g->ctx && g->ctx->gpu && cuda().ok) cuda().cuCtxSetCurrent(g->ctx->cuctx);
+  delete g;
+  return KORCH_OK;
+}
+
+korch_status korch_graph_info(const korch_graph* G, int32_t* np, int32_t* ni, int32_t* no) {
+  if (!G) return fail(KORCH_E_ARG, "NULL graph");
+  if (np) *np = (int32_t)G->g.prims.size();
+  if (ni) *ni = (int32_t)G->g.inputs.size();
+  if (no) *no = (int32_t)G->g.outputs.size();
+  return KORCH_OK;
+}
+
+static korch_status write_buf(const std::string& s, char* buf, size_t cap, size_t* needed) {
+  if (needed) *needed = s.size() + 1;
+  if (!buf || cap < s.size() + 1) return fail(KORCH_E_ARG, "buffer too small");
+  std::memcpy(buf, s.c_str(), s.size() + 1);
+  return KORCH_OK;
+}
+
+korch_status korch_graph_dump(const korch_graph* G, char* buf, size_t cap, size_t* needed) {
+  if (!G) return fail(KORCH_E_ARG, "NULL graph");
+  KORCH_TRY({ return write_buf(dump_graph(G->g), buf, cap, needed); })
+}
+
+korch_status korch_validate(const korch_graph* G, char* report, size_t cap) {
+  if (!G) return fail(KORCH_E_ARG, "NULL graph");
+  KORCH_TRY({
+    std::string r = validate_graph(G->g);
+    size_t need;
+    return write_buf(r, report, cap, &need);
+  })
+}
+
+korch_status korch_enumerate(korch_graph* G, const korch_enum_opts* o, int64_t* n_cands, int64_t* n_states) {
+  if (!G) return fail(KORCH_E_ARG, "NULL graph");
+  KORCH_TRY({
+    EnumOpts eo;
+    if (o) {
+      if (o->max_prims > 0) eo.max_prims = o->max_prims;
+      eo.keep_multi_linear = o->keep_multi_linear != 0;
+      if (o->max_states > 0) eo.max_states = o->max_states;
+    }
+    std::lock_guard<std::mutex> lk(G->mu);
+    G->cands = enumerate_candidates(G->g, eo, &G->n_states);
+    G->cs.assign(G->cands.size(), CandState());
+    for (size_t i = 0; i < G->cands.size(); ++i) ensure_planned(G, (int64_t)i);
+    G->enumerated = true;
+    G->has_plan = false;
+    if (n_cands) *n_cands = (int64_t)G->cands.size();
+    if (n_states) *n_states = G->n_states;
+    return KORCH_OK;
+  })
+}
+
+korch_status korch_candidate(const korch_graph* G, int64_t i, korch_cand_desc* d) {
+  if (!G || !d) return fail(KORCH_E_ARG, "NULL argument");
+  if (i < 0 || i >= (int64_t)G->cands.size()) return fail(KORCH_E_ARG, "candidate index out of range");
+  const Candidate& c = G->cands[i];
+  d->n_members = (int32_t)c.members.size();
+  d->members = c.members.data();
+  d->output = c.output;
+  d->n_inputs = (int32_t)c.inputs.size();
+  d->inputs = c.inputs.data();
+  d->n_graph_inputs = (int32_t)c.graph_inputs.size();
+  d->graph_inputs = c.graph_inputs.data();
+  d->klass = c.klass;
+  d->n_dense_linear = c.n_dense;
+  d->bytes = c.bytes;
+  d->flops = c.flops;
+  d->signature = c.signature.c_str();
+  return KORCH_OK;
+}
+
+korch_status korch_candidate_source(korch_graph* G, int64_t i, char* buf, size_t cap, size_t* needed) {
+  if (!G) return fail(KORCH_E_ARG, "NULL graph");
+  if (i < 0 || i >= (int64_t)G->cands.size()) return fail(KORCH_E_ARG, "candidate index out of range");
+  KORCH_TRY({
+    ensure_planned(G, i);
+    const CandState& s = G->cs[i];
+    if (s.plan.klass == KORCH_CLASS_REJECTED) return fail(KORCH_E_UNSUPPORTED, "rejected: " + s.plan.reject);
+    std::string all;
+    for (auto& v : s.plan.variants) all += "// variant: " + v.tag + "\n" + full_source(v) + "\n";
+    return write_buf(all, buf, cap, needed);
+  })
+}
+
+korch_status korch_compile(korch_graph* G, const int64_t* idx, int64_t n, int32_t threads, const char* cache_dir,
+                           int32_t* ok) {
+  if (!G || (n > 0 && !idx)) return fail(KORCH_E_ARG, "NULL argument");
+  KORCH_TRY({
+    std::vector<int64_t> v(idx, idx + n);
+    for (auto i : v)
+      if (i < 0 || i >= (int64_t)G->cands.size()) return fail(KORCH_E_ARG, "candidate index out of range");
+    std::string cd = cache_dir ? cache_dir : default_cache_dir();
+    compile_many(G, v, threads, cd);
+    bool all_ok = true;
+    std::string first_err;
+    for (int64_t k = 0; k < n; ++k) {
+      const CandState& s = G->cs[v[k]];
+      bool good = s.plan.klass != KORCH_CLASS_REJECTED;
+      for (auto& var : s.plan.variants) {
+        Module* m = G->ctx->module_for(var.name);
+        if (!m->compiled) {
+          good = false;
+          if (first_err.empty()) first_err = var.name + ": " + m->log;
+        }
+      }
+      if (ok) ok[k] = good ? 1 : 0;
+      if (s.plan.klass != KORCH_CLASS_REJECTED && !good) all_ok = false;
+    }
+    if (!all_ok) return fail(KORCH_E_NVRTC, first_err);
+    return KORCH_OK;
+  })
+}
+
+korch_status korch_profile(korch_graph* G, const int64_t* idx, int64_t n, const korch_prof_opts* po, int64_t* cost) {
+  if (!G || (n > 0 && (!idx || !cost))) return fail(KORCH_E_ARG, "NULL argument");
+  KORCH_TRY({
+    korch_ctx* ctx = G->ctx;
+    ctx->bind();
+    int warmup = po && po->warmup > 0 ? po->warmup : 3;
+    int launches = po && po->launches > 0 ? po->launches : 20;
+    int trials = po && po->trials > 0 ? po->trials : 5;
+    bool flush = po && po->flush_l2;
+    bool tune = !po || po->tune >= 0;
+    int threads = po && po->compile_threads > 0 ? po->compile_threads : 0;
+    std::vector<int64_t> v(idx, idx + n);
+    for (auto i : v)
+      if (i < 0 || i >= (int64_t)G->cands.size()) return fail(KORCH_E_ARG, "candidate index out of range");
+    compile_many(G, v, threads, default_cache_dir());
+    CudaApi& cu = cuda();
+    if (flush && !ctx->flush) {
+      ctx->flush_bytes = std::max<size_t>((size_t)ctx->l2_bytes * 2, (size_t)256 << 20);
+      CUresult r = cu.cuMemAlloc(&ctx->flush, ctx->flush_bytes);
+      if (r != CUDA_SUCCESS) throw KorchError(KORCH_E_OOM, "flush buffer: " + cu_err(r));
+    }
+    CUevent e0, e1;
+    CU_CHECK(cu.cuEventCreate(&e0, CU_EVENT_DEFAULT));
+    CU_CHECK(cu.cuEventCreate(&e1, CU_EVENT_DEFAULT));
+    for (int64_t k = 0; k < n; ++k) {
+      int64_t ci = v[k];
+      CandState& s = G->cs[ci];
+      cost[k] = INT64_MAX;
+      if (s.plan.klass == KORCH_CLASS_REJECTED) { s.cost_ns = INT64_MAX; continue; }
+      // scratch buffers at the candidate's exact shapes
+      std::vector<size_t> offs;
+      size_t tot = 0;
+      for (auto& r : s.plan.ext) {
+        offs.push_back(tot);
+        tot += ((size_t)tensor_bytes(G->g, r) + 255) & ~(size_t)255;
+      }
+      size_t out_off = tot;
+      tot += ((size_t)tensor_bytes(G->g, Ref{false, G->cands[ci].output}) + 255) & ~(size_t)255;
+      CUdeviceptr base = ctx->arena_get(tot);
+      std::vector<const void*> ins;
+      for (size_t e = 0; e < s.plan.ext.size(); ++e) {
+        const Ref& r = s.plan.ext[e];
+        CUdeviceptr p = base + offs[e];
+        size_t ne = (size_t)numel(G->g.shape_of(r));
+        if (G->g.dtype_of(r) == DType::F32) CU_CHECK(cu.cuMemsetD32Async(p, 0x3f800000u, ne, ctx->pstream));
+        else CU_CHECK(cu.cuMemsetD16Async(p, 0x3f80, ne, ctx->pstream));
+        ins.push_back((const void*)p);
+      }
+      void* outp = (void*)(base + out_off);
+      int64_t best = INT64_MAX;
+      int bestv = -1;
+      int nv = tune ? (int)s.plan.variants.size() : 1;
+      for (int vi = 0; vi < nv; ++vi) {
+        Module* m = ctx->module_for(s.plan.variants[vi].name);
+        if (!m->compiled) continue;
+        try {
+          int nl = flush ? 1 : launches;
+          CU_CHECK(cu.cuStreamBeginCapture(ctx->pstream, CU_STREAM_CAPTURE_MODE_THREAD_LOCAL));
+          try {
+            for (int l = 0; l < nl; ++l) launch_variant(ctx, s.plan, vi, ins, outp, ctx->pstream);
+          } catch (...) {
+            CUgraph tmp;
+            cu.cuStreamEndCapture(ctx->pstream, &tmp);
+            if (tmp) cu.cuGraphDestroy(tmp);
+            throw;
+          }
+          CUgraph graph;
+          CU_CHECK(cu.cuStreamEndCapture(ctx->pstream, &graph));
+          CUgraphExec ge;
+          CU_CHECK(cu.cuGraphInstantiateWithFlags(&ge, graph, 0));
+          cu.cuGraphDestroy(graph);
+          for (int w = 0; w < warmup; ++w) CU_CHECK(cu.cuGraphLaunch(ge, ctx->pstream));
+          std::vector<float> ts;
+          for (int t = 0; t < trials; ++t) {
+            if (flush) CU_CHECK(cu.cuMemsetD8Async(ctx->flush, (unsigned char)t, ctx->flush_bytes, ctx->pstream));
+            CU_CHECK(cu.cuEventRecord(e0, ctx->pstream));
+            CU_CHECK(cu.cuGraphLaunch(ge, ctx->pstream));
+            CU_CHECK(cu.cuEventRecord(e1, ctx->pstream));
+            CU_CHECK(cu.cuEventSynchronize(e1));
+            float ms = 0;
+            CU_CHECK(cu.cuEventElapsedTime(&ms, e0, e1));
+            ts.push_back(ms / nl);
+          }
+          cu.cuGraphExecDestroy(ge);
+          std::sort(ts.begin(), ts.end());
+          int64_t ns = (int64_t)std::llround((double)ts[ts.size() / 2] * 1e6);
+          if (ns < 1) ns = 1;
+          if (ns < best) { best = ns; bestv = vi; }
+        } catch (KorchError& e) {
+          // a variant that fails to launch is rejected (cost = inf for it)
+          g_err = e.what();
+          CUresult r = cu.cuStreamSynchronize(ctx->pstream);
+          if (r != CUDA_SUCCESS) { cu.cuEventDestroy(e0); cu.cuEventDestroy(e1); throw; }
+        }
+      }
+      s.best = bestv;
+      s.cost_ns = best;
+      cost[k] = best;
+    }
+    cu.cuEventDestroy(e0);
+    cu.cuEventDestroy(e1);
+    return KORCH_OK;
+  })
+}
+
+korch_status korch_set_orchestration(korch_graph* G, const int64_t* sel, int64_t n, size_t* ws) {
+  if (!G || (n > 0 && !sel)) return fail(KORCH_E_ARG, "NULL argument");
+  KORCH_TRY({
+    std::lock_guard<std::mutex> lk(G->mu);
+    const Graph& g = G->g;
+    std::vector<int64_t> order(sel, sel + n);
+    for (auto i : order)
+      if (i < 0 || i >= (int64_t)G->cands.size()) return fail(KORCH_E_ARG, "candidate index out of range");
+    // A6: order by topological index of the output, ties by candidate index
+    std::sort(order.begin(), order.end(), [&](int64_t a, int64_t b) {
+      int ta = g.topo_index[G->cands[a].output], tb = g.topo_index[G->cands[b].output];
+      return ta != tb ? ta < tb : a < b;
+    });
+    std::vector<int64_t> uniq;
+    std::vector<int> producer(g.prims.size(), -1);  // prim -> step index
+    for (auto i : order) {
+      int o = G->cands[i].output;
+      if (producer[o] >= 0) continue;  // A7: earliest producer binds
+      producer[o] = (int)uniq.size();
+      uniq.push_back(i);
+    }
+    // Eq. 4: every input of a kernel is produced by an earlier kernel
+    for (size_t s = 0; s < uniq.size(); ++s)
+      for (int p : G->cands[uniq[s]].inputs)
+        if (producer[p] < 0 || producer[p] >= (int)s)
+          return fail(KORCH_E_INFEASIBLE, "Eq. 4 violated: kernel " + std::to_string(uniq[s]) + " needs p" +
+                                              std::to_string(p) + " which no earlier selected kernel produces");
+    // Eq. 3: every output primitive is produced
+    for (int t : g.outputs)
+      if (producer[t] < 0) return fail(KORCH_E_INFEASIBLE, "Eq. 3 violated: output p" + std::to_string(t) + " not produced");
+    for (auto i : uniq) {
+      ensure_planned(G, i);
+      if (G->cs[i].plan.klass == KORCH_CLASS_REJECTED)
+        return fail(KORCH_E_NOT_SCHEDULABLE, "candidate " + std::to_string(i) + " is rejected: " + G->cs[i].plan.reject);
+    }
+    compile_many(G, uniq, 0, default_cache_dir());
+    for (auto i : uniq) {
+      const CandState& cs = G->cs[i];
+      const KernelVariant& v = cs.plan.variants[cs.best >= 0 ? cs.best : 0];
+      Module* m = G->ctx->module_for(v.name);
+      if (!m->compiled) return fail(KORCH_E_NVRTC, v.name + ": " + m->log);
+    }
+    // liveness-based workspace plan
+    std::vector<int> last_use(g.prims.size(), -1);
+    for (size_t s = 0; s < uniq.size(); ++s)
+      for (int p : G->cands[uniq[s]].inputs) last_use[p] = std::max(last_use[p], (int)s);
+    std::map<int, int> out_index;
+    for (size_t k = 0; k < g.outputs.size(); ++k)
+      if (!out_index.count(g.outputs[k])) out_index[g.outputs[k]] = (int)k;
+    struct Blk { size_t off, size; };
+    std::vector<Blk> free_list;
+    size_t top = 0;
+    std::vector<size_t> off_of(g.prims.size(), 0);
+    auto alloc = [&](size_t bytes) {
+      bytes = (bytes + 255) & ~(size_t)255;
+      for (size_t f = 0; f < free_list.size(); ++f)
+        if (free_list[f].size >= bytes) {
+          size_t o = free_list[f].off;
+          free_list[f].off += bytes;
+          free_list[f].size -= bytes;
+          if (!free_list[f].size) free_list.erase(free_list.begin() + f);
+          return o;
+        }
+      size_t o = top;
+      top += bytes;
+      return o;
+    };
+    auto release = [&](size_t off, size_t bytes) {
+      bytes = (bytes + 255) & ~(size_t)255;
+      free_list.push_back({off, bytes});
+      std::sort(free_list.begin(), free_list.end(), [](const Blk& a, const Blk& b) { return a.off < b.off; });
+      for (size_t f = 0; f + 1 < free_list.size();) {
+        if (free_list[f].off + free_list[f].size == free_list[f + 1].off) {
+          free_list[f].size += free_list[f + 1].size;
+          free_list.erase(free_list.begin() + f + 1);
+        } else ++f;
+      }
+    };
+    std::vector<Step> steps;
+    for (size_t s = 0; s < uniq.size(); ++s) {
+      int64_t ci = uniq[s];
+      CandState& cs = G->cs[ci];
+      Step st;
+      st.cand = (int)ci;
+      st.variant = cs.best >= 0 ? cs.best : 0;
+      for (auto& r : cs.plan.ext) {
+        BufRef b;
+        if (r.is_input) { b.kind = BufRef::Input; b.index = r.id; }
+        else if (out_index.count(r.id)) { b.kind = BufRef::Output; b.index = out_index[r.id]; }
+        else { b.kind = BufRef::Work; b.offset = off_of[r.id]; }
+        st.args.push_back(b);
+      }
+      int o = G->cands[ci].output;
+      if (out_index.count(o)) { st.out.kind = BufRef::Output; st.out.index = out_index[o]; }
+      else {
+        off_of[o] = alloc((size_t)tensor_bytes(g, Ref{false, o}));
+        st.out.kind = BufRef::Work;
+        st.out.offset = off_of[o];
+      }
+      // free tensors whose last consumer is this step
+      for (int p : G->cands[ci].inputs)
+        if (last_use[p] == (int)s && !out_index.count(p)) release(off_of[p], (size_t)tensor_bytes(g, Ref{false, p}));
+      steps.push_back(st);
+    }
+    G->steps = steps;
+    G->ws_bytes = top;
+    G->has_plan = true;
+    if (G->gexec && cuda().ok) { cuda().cuGraphExecDestroy(G->gexec); G->gexec = nullptr; }
+    G->cap_ptrs.clear();
+    if (ws) *ws = top;
+    return KORCH_OK;
+  })
+}
+
+korch_status korch_plan(const korch_graph* G, int64_t* nk, int64_t* order) {
+  if (!G || !nk) return fail(KORCH_E_ARG, "NULL argument");
+  if (!G->has_plan) return fail(KORCH_E_ARG, "no accepted orchestration");
+  *nk = (int64_t)G->steps.size();
+  if (order)
+    for (size_t i = 0; i < G->steps.size(); ++i) order[i] = G->steps[i].cand;
+  return KORCH_OK;
+}
+
+korch_status korch_execute(korch_graph* G, const void* const* inputs, void* const* outputs, void* workspace,
+                           void* stream) {
+  if (!G) return fail(KORCH_E_ARG, "NULL graph");
+  if (!G->has_plan) return fail(KORCH_E_ARG, "no accepted orchestration (call korch_set_orchestration)");
+  KORCH_TRY({
+    korch_ctx* ctx = G->ctx;
+    ctx->bind();
+    CudaApi& cu = cuda();
+    std::lock_guard<std::mutex> lk(G->mu);
+    const Graph& g = G->g;
+    std::vector<const void*> ptrs;
+    for (size_t i = 0; i < g.inputs.size(); ++i) ptrs.push_back(inputs[i]);
+    for (size_t i = 0; i < g.outputs.size(); ++i) ptrs.push_back(outputs[i]);
+    ptrs.push_back(workspace);
+    if (!G->gexec || ptrs != G->cap_ptrs) {
+      if (G->gexec) { cu.cuGraphExecDestroy(G->gexec); G->gexec = nullptr; }
+      auto resolve = [&](const BufRef& b) -> void* {
+        if (b.kind == BufRef::Input) return const_cast<void*>(inputs[b.index]);
+        if (b.kind == BufRef::Output) return outputs[b.index];
+        return static_cast<char*>(workspace) + b.offset;
+      };
+      CU_CHECK(cu.cuStreamBeginCapture(ctx->pstream, CU_STREAM_CAPTURE_MODE_THREAD_LOCAL));
+      try {
+        for (auto& st : G->steps) {
+          std::vector<const void*> ins;
+          for (auto& a : st.args) ins.push_back(resolve(a));
+          launch_variant(ctx, G->cs[st.cand].plan, st.variant, ins, resolve(st.out), ctx->pstream);
+        }
+      } catch (...) {
+        CUgraph tmp = nullptr;
+        cu.cuStreamEndCapture(ctx->pstream, &tmp);
+        if (tmp) cu.cuGraphDestroy(tmp);
+        throw;
+      }
+      CUgraph graph;
+      CU_CHECK(cu.cuStreamEndCapture(ctx->pstream, &graph));
+      CU_CHECK(cu.cuGraphInstantiateWithFlags(&G->gexec, graph, 0));
+      cu.cuGraphDestroy(graph);
+      G->cap_ptrs = ptrs;
+    }
+    CU_CHECK(cu.cuGraphLaunch(G->gexec, (CUstream)stream));
+    return KORCH_OK;
+  })
+}
+
+}  // extern "C"

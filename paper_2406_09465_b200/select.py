@@ -1,0 +1,82 @@
+"""Kernel orchestration optimizer: the BLP of P:377-413, solved host-side.
+
+This is caller-side code, not the hot path: the library exports
+candidates and costs, this module picks u, and korch_set_orchestration accepts it.
+
+  minimise   sum_i c_i u_i                                  (Eq. 2)
+  s.t.       sum_i O_ij u_i >= 1          for p_j in T       (Eq. 3)
+             sum_i O_ij u_i >= I_kj u_k   for all j, k       (Eq. 4)
+with O_ij = 1 iff p_j is the materialised output of K_i (reading A2) and I_kj = 1
+iff p_j is an input of K_k.  Solved with HiGHS (scipy.optimize.milp) in place of
+PuLP/CBC (not installed).  Costs are integer nanoseconds; the objective
+c_i*(M+1) + 1 breaks ties toward fewer kernels (reading A8).
+"""
+from __future__ import annotations
+
+import numpy as np
+from scipy.optimize import Bounds, LinearConstraint, milp
+from scipy.sparse import coo_matrix
+
+INF = (1 << 63) - 1
+
+
+def solve_blp(cands, costs, outputs, time_limit=600.0):
+    """cands: list of dicts with 'output' and 'inputs'; costs: int ns (INF = rejected).
+
+    Returns (objective_ns, sorted list of selected candidate indices)."""
+    live = [i for i, c in enumerate(costs) if c < INF]
+    idx = {i: k for k, i in enumerate(live)}
+    m = len(live)
+    producers = {}
+    for i in live:
+        producers.setdefault(cands[i]["output"], []).append(idx[i])
+    rows, cols, vals, lb = [], [], [], []
+    r = 0
+    for t in outputs:                                          # Eq. 3
+        ps = producers.get(t, [])
+        if not ps:
+            raise ValueError(f"infeasible: output p{t} has no generable producer")
+        for k in ps:
+            rows.append(r); cols.append(k); vals.append(1.0)
+        lb.append(1.0)
+        r += 1
+    for i in live:                                             # Eq. 4
+        k = idx[i]
+        for j in cands[i]["inputs"]:
+            ps = producers.get(j, [])
+            for p in ps:
+                rows.append(r); cols.append(p); vals.append(1.0)
+            rows.append(r); cols.append(k); vals.append(-1.0)
+            lb.append(0.0)
+            r += 1
+    a = coo_matrix((vals, (rows, cols)), shape=(r, m)).tocsr()
+    c = np.array([float(costs[i]) * (m + 1) + 1.0 for i in live])
+    res = milp(c, integrality=np.ones(m), bounds=Bounds(0, 1),
+               constraints=LinearConstraint(a, np.array(lb), np.inf),
+               options={"time_limit": time_limit, "mip_rel_gap": 0.0})
+    if res.x is None:
+        raise RuntimeError(f"HiGHS failed: {res.message}")
+    sel = sorted(live[k] for k in range(m) if res.x[k] > 0.5)
+    return int(sum(costs[i] for i in sel)), sel
+
+
+def operator_aligned(cands, prim_graph):
+    """The 'one kernel per unfused operator' orchestration: for every
+    operator, the candidate whose members are exactly that operator's fission fragment."""
+    by_op = {}
+    for n in prim_graph["nodes"]:
+        by_op.setdefault(n["op"], []).append(n["id"])
+    key = {tuple(c["members"]): i for i, c in enumerate(cands)}
+    sel = []
+    for op, members in sorted(by_op.items()):
+        i = key.get(tuple(sorted(members)))
+        if i is None:
+            raise ValueError(f"operator {op}'s fragment {members} is not a candidate")
+        sel.append(i)
+    return sorted(sel)
+
+
+def singletons(cands, n_prims):
+    """One kernel per primitive (the fully unfused orchestration)."""
+    key = {tuple(c["members"]): i for i, c in enumerate(cands)}
+    return sorted(key[(p,)] for p in range(n_prims))

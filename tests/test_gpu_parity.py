@@ -1,0 +1,178 @@
+"""GPU parity: the CUDA path (through the C ABI) against the oracle, element by element,
+on the same seeded inputs.  Tolerances (BASELINE.json north star, reading A21):
+per output tensor ||gpu - oracle||_inf <= rtol * ||oracle||_inf, rtol = 1e-4 (fp32
+storage) / 2e-2 (bf16 storage); layout-only graphs bit-exact."""
+import numpy as np
+import pytest
+
+from korch_workloads import c1_softmax_layernorm, c2_vit_attention, make_inputs
+from korch_workloads.graphs import GraphBuilder
+from oracle.enumeration import PGraph, candidates, convex_sets_from_states, execution_states
+from oracle.evaluate import eval_orchestration, eval_primitive_graph
+from oracle.fission import fission
+
+torch = pytest.importorskip("torch")
+
+RTOL = {"f32": 1e-4, "bf16": 2e-2}
+
+
+@pytest.fixture(scope="module")
+def ctx():
+    from paper_2406_09465_b200 import Context
+    return Context(0)
+
+
+class Case:
+    """One graph loaded both ways: the library (device) and the oracle (host, fp64)."""
+
+    def __init__(self, ctx, graph, seed=0, max_prims=16):
+        from paper_2406_09465_b200 import KorchGraph, torch_inputs
+        self.graph = graph
+        self.kg = KorchGraph(ctx, graph)
+        self.cands = self.kg.enumerate(max_prims=max_prims)
+        self.pg = fission(graph)
+        self.G = PGraph(self.pg)
+        self.ref = candidates(self.G, convex_sets_from_states(execution_states(self.G)), max_prims=max_prims)
+        assert [(tuple(c["members"]), c["output"]) for c in self.cands] == [(tuple(m), o) for m, o in self.ref]
+        ins = make_inputs(graph, seed=seed)
+        self.values = {k: v[0] for k, v in ins.items()}
+        self.dev_in = torch_inputs(graph, {k: v[1] for k, v in ins.items()})
+        self.storage = graph["dtype"]
+
+    def completion(self, must):
+        """A feasible selection containing `must`, completed with generable producers."""
+        gen = {c["index"] for c in self.cands if c["klass"] != "rejected"}
+        prod = {}
+        for c in self.cands:
+            if c["index"] in gen:
+                prod.setdefault(c["output"], []).append(c["index"])
+        for o in prod:  # prefer the smallest producer
+            prod[o].sort(key=lambda i: (len(self.cands[i]["members"]), i))
+        sel, have = list(must), {self.cands[i]["output"] for i in must}
+        need = [j for i in must for j in self.cands[i]["inputs"]] + list(self.kg.outputs)
+        while need:
+            t = need.pop()
+            if t in have:
+                continue
+            i = prod[t][0]
+            sel.append(i)
+            have.add(t)
+            need.extend(self.cands[i]["inputs"])
+        return sorted(set(sel))
+
+    def run(self, sel):
+        self.kg.set_orchestration(sel)
+        outs = self.kg.torch_outputs()
+        ws = self.kg.torch_workspace()
+        self.kg.execute(self.dev_in, outs, ws, torch.cuda.current_stream())
+        torch.cuda.synchronize()
+        return [o.float().cpu().numpy().astype(np.float64) for o in outs]
+
+    def oracle(self, sel):
+        return eval_orchestration(self.pg, self.ref, sel, self.values, self.G.topo_index, self.storage)
+
+    def check(self, sel, rtol=None, exact=False):
+        got = self.run(sel)
+        ref = self.oracle(sel)
+        rtol = RTOL[self.storage] if rtol is None else rtol
+        for k, o in enumerate(self.kg.outputs):
+            r = ref[o]
+            assert got[k].shape == r.shape
+            if exact:
+                np.testing.assert_array_equal(got[k], r)
+            else:
+                err = np.max(np.abs(got[k] - r))
+                scale = np.max(np.abs(r))
+                assert err <= rtol * scale, f"sel={sel}: err {err:.3e} > {rtol} * {scale:.3e}"
+        return got, ref
+
+
+@pytest.mark.gpu
+def test_c1_every_candidate(ctx):
+    """Every C1 candidate kernel (all 120) runs inside a feasible orchestration and matches."""
+    c = Case(ctx, c1_softmax_layernorm())
+    gen = [x["index"] for x in c.cands if x["klass"] != "rejected"]
+    assert len(gen) == len(c.cands) == 120
+    for i in gen:
+        c.check(c.completion([i]))
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("rows,cols", [(4, 128), (1000, 128), (37, 100), (3, 2048), (5, 4096), (64, 96)])
+def test_c1_shapes_whole_and_singletons(ctx, rows, cols):
+    """Several tiles, ragged tails (masked rows), block-reduce rows (> 32 threads)."""
+    c = Case(ctx, c1_softmax_layernorm(rows=rows, cols=cols))
+    whole = [x["index"] for x in c.cands if len(x["members"]) == c.kg.n_prims]
+    c.check(whole)
+    c.check(c.kg.singletons())
+    c.check(c.kg.operator_aligned())
+
+
+@pytest.mark.gpu
+def test_c1_invariants_on_gpu(ctx):
+    """Softmax rows sum to 1 (fp32 <= 1e-5) and LayerNorm (eps=0, no affine) has mean 0 / var 1."""
+    g = c1_softmax_layernorm(rows=64, cols=128, affine=False, eps=0.0)
+    c = Case(ctx, g)
+    whole = [x["index"] for x in c.cands if len(x["members"]) == c.kg.n_prims][0]
+    y = c.run([whole])[0]
+    np.testing.assert_allclose(y.mean(1), 0, atol=1e-5)
+    np.testing.assert_allclose(y.var(1), 1, atol=1e-4)
+    g2 = GraphBuilder("f32")
+    x = g2.input("x", [64, 128])
+    g2.output(g2.op("Softmax", x, axis=1))
+    c2 = Case(ctx, g2.build())
+    s = c2.run(c2.kg.singletons())[0]
+    np.testing.assert_allclose(s.sum(1), 1, atol=1e-5)
+
+
+@pytest.mark.gpu
+def test_full_pipeline_c1(ctx):
+    """enumerate -> profile -> BLP -> execute; the chosen orchestration matches the oracle
+    and its cost is no worse than the operator-aligned baseline's."""
+    c = Case(ctx, c1_softmax_layernorm())
+    costs = c.kg.profile()
+    assert all(0 < x < (1 << 62) for x in costs)
+    obj, sel = c.kg.select(costs)
+    base = c.kg.operator_aligned()
+    assert obj <= sum(costs[i] for i in base)
+    c.check(sel)
+
+
+def _layout_graph(dtype):
+    b = GraphBuilder(dtype)
+    x = b.input("x", [4, 6, 8, 16])
+    y = b.op("Transpose", x, perm=[0, 2, 1, 3])
+    y = b.op("Reshape", y, shape=[32, 96])
+    y = b.op("Slice", y, axis=1, start=16, end=80)
+    y = b.op("Pad", y, pads=[[1, 0], [0, 2]], mode="constant", value=0.0)
+    y = b.op("Transpose", y, perm=[1, 0])
+    b.output(y)
+    return b.build()
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("dtype", ["f32", "bf16"])
+def test_layout_only_bit_exact(ctx, dtype):
+    c = Case(ctx, _layout_graph(dtype))
+    for i in [x["index"] for x in c.cands if x["klass"] != "rejected"]:
+        c.check(c.completion([i]), exact=True)
+
+
+@pytest.mark.gpu
+def test_misc_memory_bound_ops(ctx):
+    b = GraphBuilder("f32")
+    x = b.input("x", [2, 8, 10, 12])
+    g = b.input("g", [8], mean=1.0, std=0.1)
+    be = b.input("be", [8], std=0.1)
+    y = b.op("InstanceNorm", x, g, be, eps=1e-5)
+    y = b.op("Relu", y)
+    y = b.op("Pad", y, pads=[[0, 0], [0, 0], [1, 1], [1, 1]], mode="reflect")
+    y = b.op("GELU", y)
+    y = b.op("Upsample2x", y)
+    b.output(y)
+    c = Case(ctx, b.build())
+    gen = [x["index"] for x in c.cands if x["klass"] != "rejected"]
+    assert len(gen) > 0
+    for i in gen[:: max(1, len(gen) // 40)]:
+        c.check(c.completion([i]))
+    c.check(c.kg.operator_aligned())

@@ -1,0 +1,163 @@
+"""Host-side parity of the library against the oracle (bit-exact, no GPU):
+fission (primitive graph), Alg. 1 enumeration (candidate lists), BLP selection."""
+import numpy as np
+import pytest
+
+from korch_workloads import c1_softmax_layernorm, c2_vit_attention
+from korch_workloads.graphs import GraphBuilder
+from oracle.enumeration import PGraph, candidate_inputs, candidates, convex_sets_from_states, execution_states
+from oracle.fission import fission
+from oracle.orchestration import feasible, producer_search
+
+from paper_2406_09465_b200 import Context, KorchGraph, solve_blp
+
+
+@pytest.fixture(scope="module")
+def ctx():
+    return Context(-1)
+
+
+def _norm_ref(r):
+    return ("input", r["input"]) if "input" in r else ("node", r["node"])
+
+
+def _norm_attrs(kind, a):
+    a = dict(a)
+    if kind == "pad":
+        a["pads"] = [list(p) for p in a["pads"]]
+    if "c" in a:
+        a["c"] = float(np.float64(a["c"]))
+    return a
+
+
+GRAPHS = {
+    "c1": lambda: c1_softmax_layernorm(),
+    "c1_noaffine": lambda: c1_softmax_layernorm(affine=False, eps=0.0),
+    "c2": lambda: c2_vit_attention(),
+    "c2_b2": lambda: c2_vit_attention(batch=2, seq=32, hidden=128, heads=4),
+}
+
+
+def _misc_graph():
+    b = GraphBuilder("f32")
+    x = b.input("x", [2, 16, 6, 6])
+    w = b.input("w", [16, 16, 3, 3], std=0.1)
+    g = b.input("g", [16], mean=1.0, std=0.1)
+    be = b.input("be", [16], std=0.1)
+    y = b.op("Conv", x, w, stride=[1, 1], pads=[1, 1], groups=1)
+    y = b.op("InstanceNorm", y, g, be, eps=1e-5)
+    y = b.op("Relu", y)
+    y = b.op("Pad", y, pads=[[0, 0], [0, 0], [1, 1], [1, 1]], mode="reflect")
+    y = b.op("GELU", y)
+    z = b.op("Upsample2x", y)
+    b.output(z)
+    return b.build()
+
+
+GRAPHS["misc"] = _misc_graph
+
+
+@pytest.mark.parametrize("name", sorted(GRAPHS))
+def test_fission_matches_oracle(ctx, name):
+    g = GRAPHS[name]()
+    ours = KorchGraph(ctx, g).prim
+    ref = fission(g)
+    assert len(ours["nodes"]) == len(ref["nodes"])
+    for a, b in zip(ours["nodes"], ref["nodes"]):
+        assert a["id"] == b["id"]
+        assert a["kind"] == b["kind"], (a, b)
+        assert tuple(a["shape"]) == tuple(b["shape"])
+        assert [_norm_ref(r) for r in a["inputs"]] == [tuple(r) for r in b["inputs"]]
+        ra = _norm_attrs(a["kind"], a["attrs"])
+        rb = _norm_attrs(b["kind"], b["attrs"])
+        for k, v in rb.items():
+            if k == "port_axes":
+                assert {kk: list(vv) for kk, vv in ra[k].items()} == {kk: list(vv) for kk, vv in v.items()}
+            else:
+                assert ra[k] == v, (k, ra, rb)
+    assert ours["outputs"] == ref["outputs"]
+
+
+def _oracle_cands(g, max_prims=16):
+    pg = fission(g)
+    G = PGraph(pg)
+    return G, candidates(G, convex_sets_from_states(execution_states(G)), max_prims=max_prims)
+
+
+@pytest.mark.parametrize("name", sorted(GRAPHS))
+def test_enumeration_matches_oracle(ctx, name):
+    g = GRAPHS[name]()
+    kg = KorchGraph(ctx, g)
+    ours = kg.enumerate()
+    G, ref = _oracle_cands(g)
+    st = execution_states(G)
+    assert kg.n_states == len(st)
+    assert [(tuple(c["members"]), c["output"]) for c in ours] == [(tuple(m), o) for m, o in ref]
+    for c in ours:
+        assert c["inputs"] == candidate_inputs(G, c["members"])
+
+
+def _random_op_graph(rng, n_ops):
+    """Random DAG of elementwise / softmax / layout operators on [8, 32] tensors."""
+    b = GraphBuilder("f32")
+    refs = [b.input("x", [8, 32])]
+    for _ in range(n_ops):
+        k = int(rng.integers(0, 5))
+        a = refs[int(rng.integers(0, len(refs)))]
+        if k == 0:
+            r = b.op("Exp", a)
+        elif k == 1:
+            r = b.op("Add", a, refs[int(rng.integers(0, len(refs)))])
+        elif k == 2:
+            r = b.op("Softmax", a, axis=1)
+        elif k == 3:
+            r = b.op("MulC", a, c=0.5)
+        else:
+            r = b.op("Relu", a)
+        refs.append(r)
+    used = set()
+    for n in b.g["nodes"]:
+        for r in n["inputs"]:
+            if "node" in r:
+                used.add(r["node"])
+    for n in b.g["nodes"]:
+        if n["id"] not in used:
+            b.output({"node": n["id"]})
+    return b.build()
+
+
+def test_enumeration_random_graphs(ctx):
+    rng = np.random.default_rng(3)
+    for _ in range(25):
+        g = _random_op_graph(rng, int(rng.integers(2, 7)))
+        kg = KorchGraph(ctx, g)
+        ours = kg.enumerate(max_prims=8)
+        _, ref = _oracle_cands(g, max_prims=8)
+        assert [(tuple(c["members"]), c["output"]) for c in ours] == [(tuple(m), o) for m, o in ref]
+
+
+def test_blp_matches_exact_search_c1(ctx):
+    """The product's HiGHS BLP reaches exactly the oracle's producer-assignment optimum."""
+    g = c1_softmax_layernorm()
+    kg = KorchGraph(ctx, g)
+    cands = kg.enumerate()
+    G, ref = _oracle_cands(g)
+    cin = [candidate_inputs(G, m) for m, _ in ref]
+    rng = np.random.default_rng(9)
+    for _ in range(4):
+        costs = [int(1500 + 100 * len(c["members"]) + rng.integers(0, 800)) for c in cands]
+        obj, sel = solve_blp(cands, costs, kg.outputs)
+        best, osel = producer_search(ref, costs, G.pg["outputs"], cin, G.topo_index)
+        assert obj == best
+        assert feasible(ref, sel, G.pg["outputs"], cin)
+        kg.set_orchestration(sel)          # the library accepts it (Eq. 3/4)
+
+
+def test_blp_with_rejections_and_baselines(ctx):
+    g = c2_vit_attention()
+    kg = KorchGraph(ctx, g)
+    cands = kg.enumerate()
+    base = kg.operator_aligned()
+    assert len(base) == len(g["nodes"])
+    singles = kg.singletons()
+    assert len(singles) == kg.n_prims
