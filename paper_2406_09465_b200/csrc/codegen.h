@@ -29,6 +29,7 @@ struct KernelVariant {
   std::string source;
   int block = 256;
   int64_t grid = 1;
+  int64_t grid_y = 1, grid_z = 1;
   int smem = 0;             // dynamic shared memory bytes
   int cluster = 1;
   std::string tag;
@@ -45,6 +46,17 @@ struct KernelPlan {
 };
 
 KernelPlan generate_kernel(const Graph& g, const Candidate& c);
+
+// Epilogue of a GEMM candidate, emitted by the row-template machinery: `body` computes
+// the output chunk from float acc[32] (row gm, columns nb..nb+31) and `store` writes it.
+struct GemmEpilogue {
+  std::vector<Ref> ext;               // pre_ext first, then epilogue operands
+  std::string body, store;
+  int64_t bytes = 0;                  // epilogue reads + output write
+  std::vector<std::string> batch_vars;
+};
+bool make_gemm_epilogue(const Graph& g, const Candidate& c, int mm, const std::vector<Ref>& pre_ext,
+                        GemmEpilogue* out, std::string* err);
 KernelPlan generate_gemm(const Graph& g, const Candidate& c);   // gemm_gen.cpp
 std::string kernel_prelude();
 std::string fmt_float(double v);

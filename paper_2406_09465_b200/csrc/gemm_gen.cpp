@@ -1,15 +1,338 @@
-// GEMM template (KB5): placeholder until the tcgen05 kernel lands.
+// KB5: GEMM template for candidates with exactly one dense linear primitive (MatMul /
+// batched MatMul), the paper's "compute-intensive" class, re-designed for
+// sm_100a: tcgen05.mma (bf16 in, fp32 accumulate in TMEM), operands staged by TMA into a
+// 4-stage mbarrier ring with 128B swizzle, one 128 x BN tile per CTA.
+//
+// Upstream members (Transpose / Reshape / Slice chains feeding the MatMul) are folded
+// into the TMA tensor maps as strided views -- the data-layout trick of P:529-531
+// (kernel k5) without materialising the transposed operand.  Downstream members
+// (elementwise ops, port broadcasts, side-branch reads, Transpose/Reshape of the result)
+// are fused into the epilogue, emitted by the row-template machinery.
+#include <set>
+#include <sstream>
+
 #include "../../include/korch.h"
 #include "codegen.h"
+#include "expr.h"
 
 namespace korch {
 
+extern const char* kSm100GemmTemplate;  // templates/sm100_gemm.cuh (embedded by build.py)
+
+namespace {
+
+struct View {
+  Ref src;                      // external tensor
+  std::vector<int64_t> coef;    // per operand axis (batch..., row, col), elements
+  int64_t off = 0;              // element offset
+  Shape shape;                  // operand shape
+};
+
+bool operand_view(const Graph& g, const std::set<int>& mem, const Prim& L, int slot, View* v, std::set<int>* chain,
+                  std::string* err) {
+  ExprCtx X;
+  const Shape& s = g.shape_of(L.in[slot]);
+  std::vector<Lin> co;
+  std::vector<int> vars;
+  for (size_t i = 0; i < s.size(); ++i) {
+    int id = X.add_var("a" + std::to_string(i), 0, s[i] - 1);
+    vars.push_back(id);
+    co.push_back(X.var(id));
+  }
+  Ref r = L.in[slot];
+  while (!r.is_input && mem.count(r.id)) {
+    const Prim& q = g.prims[r.id];
+    chain->insert(q.id);
+    const Shape& is = g.shape_of(q.in[0]);
+    std::vector<Lin> c2;
+    if (q.kind == Kind::Transpose) {
+      c2.resize(co.size());
+      for (size_t i = 0; i < co.size(); ++i) c2[q.perm[i]] = co[i];
+    } else if (q.kind == Kind::Reshape) {
+      Lin flat = ExprCtx::cst(0);
+      int64_t st = 1;
+      for (int k = (int)q.shape.size() - 1; k >= 0; --k) {
+        flat = ExprCtx::add(flat, ExprCtx::scale(co[k], st));
+        st *= q.shape[k];
+      }
+      c2.resize(is.size());
+      st = 1;
+      for (int k = (int)is.size() - 1; k >= 0; --k) {
+        c2[k] = X.mod(X.div(flat, st), is[k]);
+        st *= is[k];
+      }
+    } else if (q.kind == Kind::Slice) {
+      c2 = co;
+      c2[q.axis] = ExprCtx::add(co[q.axis], ExprCtx::cst(q.start));
+    } else {
+      *err = std::string("'") + kind_name(q.kind) + "' upstream of the linear primitive is not a strided view";
+      return false;
+    }
+    co = c2;
+    r = q.in[0];
+  }
+  const Shape& ts = g.shape_of(r);
+  Lin addr = ExprCtx::cst(0);
+  int64_t st = 1;
+  for (int k = (int)ts.size() - 1; k >= 0; --k) {
+    addr = ExprCtx::add(addr, ExprCtx::scale(co[k], st));
+    st *= ts[k];
+  }
+  for (auto& t : addr.terms)
+    if (t.second.type != Atom::Var) {
+      *err = "operand view is not affine (layout chain does not fold into strides)";
+      return false;
+    }
+  v->src = r;
+  v->shape = s;
+  v->off = addr.c0;
+  v->coef.assign(s.size(), 0);
+  for (size_t i = 0; i < s.size(); ++i) {
+    int64_t c = 0;
+    ExprCtx::linear_in(addr, vars[i], &c);
+    v->coef[i] = c;
+  }
+  return true;
+}
+
+std::string str(int64_t v) { return std::to_string(v); }
+
+}  // namespace
+
 KernelPlan generate_gemm(const Graph& g, const Candidate& c) {
-  (void)g;
-  (void)c;
   KernelPlan kp;
   kp.klass = KORCH_CLASS_REJECTED;
-  kp.reject = "GEMM template not available";
+  int mm = -1;
+  for (int m : c.members)
+    if (g.is_dense_linear(m)) mm = m;
+  const Prim& L = g.prims[mm];
+  if (L.kind != Kind::MatMul) {
+    kp.reject = "implicit-GEMM convolution template not available";
+    return kp;
+  }
+  std::set<int> mem(c.members.begin(), c.members.end());
+  View va, vb;
+  std::set<int> chain;
+  std::string err;
+  if (!operand_view(g, mem, L, 0, &va, &chain, &err) || !operand_view(g, mem, L, 1, &vb, &chain, &err)) {
+    kp.reject = err;
+    return kp;
+  }
+  // every member upstream of L must be part of an operand view chain
+  {
+    std::vector<int> stack{mm};
+    std::set<int> anc;
+    while (!stack.empty()) {
+      int v = stack.back();
+      stack.pop_back();
+      for (int p : g.preds[v])
+        if (mem.count(p) && !anc.count(p)) {
+          anc.insert(p);
+          stack.push_back(p);
+        }
+    }
+    for (int a : anc)
+      if (!chain.count(a)) {
+        kp.reject = "computation upstream of the linear primitive (not a view)";
+        return kp;
+      }
+  }
+  if (g.dtype_of(va.src) != DType::BF16 || g.dtype_of(vb.src) != DType::BF16) {
+    kp.reject = "GEMM operands must be bf16 (tcgen05 kind::f16)";
+    return kp;
+  }
+  const Shape& C = L.shape;
+  int nbC = (int)C.size() - 2;
+  int64_t M = C[nbC], N = C[nbC + 1], K = va.shape.back();
+  int nbA = (int)va.shape.size() - 2, nbB = (int)vb.shape.size() - 2;
+  if (nbA != nbC || (nbB != 0 && nbB != nbC)) {
+    kp.reject = "unsupported batch broadcast";
+    return kp;
+  }
+  // majorness
+  int64_t a_m = va.coef[nbA], a_k = va.coef[nbA + 1], b_k = vb.coef[nbB], b_n = vb.coef[nbB + 1];
+  bool a_kmaj = a_k == 1 || K == 1, a_mmaj = !a_kmaj && (a_m == 1 || M == 1);
+  bool b_kmaj = b_k == 1 || K == 1, b_nmaj = !b_kmaj && (b_n == 1 || N == 1);
+  if (!(a_kmaj || a_mmaj) || !(b_kmaj || b_nmaj)) {
+    kp.reject = "operand has no unit-stride axis for TMA";
+    return kp;
+  }
+  if ((va.off * 2) % 16 || (vb.off * 2) % 16) {
+    kp.reject = "operand view offset not 16-byte aligned";
+    return kp;
+  }
+
+  auto build_desc = [&](const View& v, int ext_idx, int64_t inner_dim, int64_t outer_dim, int64_t outer_coef,
+                        uint32_t inner_box, uint32_t outer_box, int nbatch, std::vector<int>* batch_axes,
+                        TmaDesc* d) -> bool {
+    d->tensor = ext_idx;
+    d->dtype = 1;
+    d->swizzle = 3;
+    d->elem_off = v.off;
+    d->rank = 0;
+    auto push = [&](int64_t dim, int64_t stride_el, uint32_t box) {
+      d->dims[d->rank] = dim;
+      d->strides[d->rank] = stride_el * 2;
+      d->box[d->rank] = box;
+      d->rank++;
+    };
+    push(inner_dim, 1, inner_box);
+    push(outer_dim, outer_dim > 1 ? outer_coef : (outer_coef ? outer_coef : inner_dim), outer_box);
+    for (int b = 0; b < nbatch; ++b)
+      if (v.coef[b] != 0 && v.shape[b] > 1) {
+        if (d->rank >= 5) return false;
+        push(v.shape[b], v.coef[b], 1);
+        batch_axes->push_back(b);
+      }
+    for (int i = 1; i < d->rank; ++i)
+      if (d->strides[i] % 16 || d->strides[i] <= 0 || d->strides[i] >= (1LL << 40)) return false;
+    return true;
+  };
+
+  std::vector<Ref> pre{va.src, vb.src};
+  GemmEpilogue ep;
+  if (!make_gemm_epilogue(g, c, mm, pre, &ep, &err)) {
+    kp.reject = err;
+    return kp;
+  }
+  int slotA = 0, slotB = (va.src.is_input == vb.src.is_input && va.src.id == vb.src.id) ? 0 : 1;
+  kp.ext = ep.ext;
+  int64_t batch = 1;
+  for (int b = 0; b < nbC; ++b) batch *= C[b];
+  kp.flops = 2.0 * (double)M * (double)N * (double)K * (double)batch;
+  int64_t a_el = numel(va.shape), b_el = numel(vb.shape);
+  kp.bytes = ep.bytes + 2 * (a_el + b_el);
+
+  std::vector<int> bns;
+  for (int bn : {64, 128, 256})
+    if (bn <= 64 || bn / 2 < N) bns.push_back(bn);
+  for (int BN : bns) {
+    TmaDesc da, db;
+    std::vector<int> ba_axes, bb_axes;
+    bool ok = a_kmaj ? build_desc(va, slotA, K, M, a_m, 64, 128, nbA, &ba_axes, &da)
+                     : build_desc(va, slotA, M, K, a_k, 64, 64, nbA, &ba_axes, &da);
+    ok = ok && (b_kmaj ? build_desc(vb, slotB, K, N, b_n, 64, (uint32_t)BN, nbB, &bb_axes, &db)
+                       : build_desc(vb, slotB, N, K, b_k, 64, 64, nbB, &bb_axes, &db));
+    if (!ok) {
+      kp.reject = "operand strides not expressible as a TMA tensor map";
+      continue;
+    }
+    const int S = 4;
+    const int A_BYTES = 128 * 64 * 2, B_BYTES = BN * 64 * 2, STAGE = A_BYTES + B_BYTES;
+    const int smem = S * STAGE + 1024 + (2 * S + 1) * 8 + 16;
+    const int64_t NK = (K + 63) / 64;
+    const int tcols = BN < 32 ? 32 : BN;
+    uint32_t idesc = (1u << 4) | (1u << 7) | (1u << 10) | ((a_kmaj ? 0u : 1u) << 15) | ((b_kmaj ? 0u : 1u) << 16) |
+                     ((uint32_t)(BN >> 3) << 17) | ((uint32_t)(128 >> 4) << 24);
+    auto coords = [&](const std::string& inner, const std::string& outer, const std::vector<int>& baxes) {
+      std::string s = inner + ", " + outer;
+      for (int b : baxes) s += ", " + ep.batch_vars[b];
+      return s;
+    };
+    auto load = [&](int rank) { return "tma_load_" + std::to_string(rank) + "d"; };
+    std::ostringstream k;
+    k << "extern \"C\" __global__ void __launch_bounds__(128, 1) KNAME(";
+    for (size_t i = 0; i < kp.ext.size(); ++i)
+      k << "const " << (g.dtype_of(kp.ext[i]) == DType::F32 ? "float" : "bf16_t") << "* __restrict__ p" << i << ", ";
+    k << (g.prims[c.output].dtype == DType::F32 ? "float" : "bf16_t") << "* __restrict__ out, "
+      << "const __grid_constant__ TmaMap tmA, const __grid_constant__ TmaMap tmB) {\n";
+    k << "  typedef int idx_t;\n";
+    k << "  extern __shared__ __align__(1024) unsigned char smem_raw[];\n";
+    k << "  unsigned char* smem = (unsigned char*)(((unsigned long long)smem_raw + 1023ull) & ~1023ull);\n";
+    k << "  unsigned long long* full = (unsigned long long*)(smem + " << S * STAGE << ");\n";
+    k << "  unsigned long long* empty = full + " << S << ";\n";
+    k << "  unsigned long long* accf = empty + " << S << ";\n";
+    k << "  unsigned* tslot = (unsigned*)(accf + 1);\n";
+    k << "  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;\n";
+    k << "  const int tile_m = blockIdx.x * 128, tile_n = blockIdx.y * " << BN << ";\n";
+    k << "  int bzl = blockIdx.z;\n";
+    for (int b = nbC - 1; b >= 0; --b) {
+      k << "  const int " << ep.batch_vars[b] << " = bzl % " << C[b] << "; bzl /= " << C[b] << ";\n";
+    }
+    k << "  (void)bzl;\n";
+    k << "  if (threadIdx.x == 0) {\n    for (int s = 0; s < " << S
+      << "; ++s) { mbar_init(full + s, 1); mbar_init(empty + s, 1); }\n"
+      << "    mbar_init(accf, 1);\n    mbar_fence_init();\n    tma_prefetch(&tmA);\n    tma_prefetch(&tmB);\n  }\n";
+    k << "  if (warp == 2) tc_alloc(tslot, " << tcols << ");\n";
+    k << "  tc_fence_before();\n  __syncthreads();\n  tc_fence_after();\n";
+    k << "  const unsigned tmem = *tslot;\n";
+    // producer
+    k << "  if (warp == 0 && lane == 0) {\n";
+    k << "    int s = 0; unsigned ph = 0;\n";
+    k << "    for (int kb = 0; kb < " << NK << "; ++kb) {\n";
+    k << "      mbar_wait(empty + s, ph ^ 1u);\n";
+    k << "      mbar_expect_tx(full + s, " << STAGE << "u);\n";
+    k << "      unsigned char* sa = smem + s * " << STAGE << ";\n";
+    k << "      unsigned char* sb = sa + " << A_BYTES << ";\n";
+    if (a_kmaj) {
+      k << "      " << load(da.rank) << "(sa, &tmA, full + s, " << coords("kb * 64", "tile_m", ba_axes) << ");\n";
+    } else {
+      for (int cc = 0; cc < 2; ++cc)
+        k << "      " << load(da.rank) << "(sa + " << cc * 8192 << ", &tmA, full + s, "
+          << coords("tile_m + " + str(cc * 64), "kb * 64", ba_axes) << ");\n";
+    }
+    if (b_kmaj) {
+      k << "      " << load(db.rank) << "(sb, &tmB, full + s, " << coords("kb * 64", "tile_n", bb_axes) << ");\n";
+    } else {
+      for (int cc = 0; cc < BN / 64; ++cc)
+        k << "      " << load(db.rank) << "(sb + " << cc * 8192 << ", &tmB, full + s, "
+          << coords("tile_n + " + str(cc * 64), "kb * 64", bb_axes) << ");\n";
+    }
+    k << "      if (++s == " << S << ") { s = 0; ph ^= 1u; }\n    }\n";
+    // MMA issuer
+    k << "  } else if (warp == 1 && lane == 0) {\n";
+    k << "    int s = 0; unsigned ph = 0;\n";
+    k << "    for (int kb = 0; kb < " << NK << "; ++kb) {\n";
+    k << "      mbar_wait(full + s, ph);\n      tc_fence_after();\n";
+    k << "      const unsigned sa = smem_u32(smem + s * " << STAGE << "), sb = sa + " << A_BYTES << ";\n";
+    k << "      #pragma unroll\n      for (int k = 0; k < 4; ++k) {\n";
+    k << "        const unsigned long long ad = umma_desc(sa + " << (a_kmaj ? "k * 32" : "k * 2048") << ", "
+      << (a_kmaj ? 16 : 8192) << ", 1024);\n";
+    k << "        const unsigned long long bd = umma_desc(sb + " << (b_kmaj ? "k * 32" : "k * 2048") << ", "
+      << (b_kmaj ? 16 : 8192) << ", 1024);\n";
+    k << "        tc_mma(tmem, ad, bd, " << idesc << "u, (kb | k) != 0);\n      }\n";
+    k << "      tc_commit(empty + s);\n";
+    k << "      if (++s == " << S << ") { s = 0; ph ^= 1u; }\n    }\n";
+    k << "    tc_commit(accf);\n  }\n";
+    // epilogue
+    k << "  __syncwarp();\n  mbar_wait(accf, 0);\n  __syncwarp();\n  tc_fence_after();\n";
+    k << "  {\n    const int gm = tile_m + warp * 32 + lane;\n    const int tid = 0;\n    (void)tid;\n";
+    k << "    #pragma unroll 1\n    for (int ch = 0; ch < " << BN / 32 << "; ++ch) {\n";
+    k << "      const int nb = tile_n + ch * 32;\n";
+    k << "      float acc[32];\n";
+    k << "      tc_ld32(tmem + ((unsigned)(warp * 32) << 16) + (unsigned)(ch * 32), acc);\n";
+    k << "      if (gm < " << M << " && nb < " << N << ") {\n";
+    k << ep.body << ep.store;
+    k << "      }\n    }\n  }\n";
+    k << "  tc_fence_before();\n  __syncthreads();\n";
+    k << "  if (warp == 2) tc_dealloc(tmem, " << tcols << ");\n}\n";
+
+    KernelVariant kv;
+    std::string src = std::string(kSm100GemmTemplate) + "\n" + k.str();
+    char nm[64];
+    std::snprintf(nm, sizeof nm, "korch_gemm_%016llx", (unsigned long long)fnv1a(src));
+    kv.name = nm;
+    size_t pos = src.find("KNAME");
+    src.replace(pos, 5, kv.name);
+    kv.source = src;
+    kv.block = 128;
+    kv.grid = 0;
+    kv.grid_y = (N + BN - 1) / BN;
+    kv.grid_z = batch;
+    kv.grid = (M + 127) / 128;
+    kv.smem = smem;
+    da.tensor = slotA;
+    db.tensor = slotB;
+    kv.tma = {da, db};
+    std::ostringstream t;
+    t << "gemm BM=128 BN=" << BN << " BK=64 stages=" << S << " A=" << (a_kmaj ? "K" : "M") << "-major B="
+      << (b_kmaj ? "K" : "N") << "-major M=" << M << " N=" << N << " K=" << K << " batch=" << batch;
+    kv.tag = t.str();
+    kp.variants.push_back(kv);
+  }
+  if (kp.variants.empty()) return kp;
+  kp.klass = KORCH_CLASS_GEMM;
+  kp.reject.clear();
   return kp;
 }
 

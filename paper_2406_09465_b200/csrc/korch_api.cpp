@@ -301,7 +301,8 @@ static void launch_variant(korch_ctx* ctx, const KernelPlan& plan, int vi, const
   if (v.cluster > 1) {
     CUlaunchConfig cfg{};
     cfg.gridDimX = (unsigned)v.grid;
-    cfg.gridDimY = cfg.gridDimZ = 1;
+    cfg.gridDimY = (unsigned)v.grid_y;
+    cfg.gridDimZ = (unsigned)v.grid_z;
     cfg.blockDimX = (unsigned)v.block;
     cfg.blockDimY = cfg.blockDimZ = 1;
     cfg.sharedMemBytes = (unsigned)v.smem;
@@ -314,7 +315,7 @@ static void launch_variant(korch_ctx* ctx, const KernelPlan& plan, int vi, const
     cfg.numAttrs = 1;
     CU_CHECK(cuda().cuLaunchKernelEx(&cfg, fn, args.data(), nullptr));
   } else {
-    CU_CHECK(cuda().cuLaunchKernel(fn, (unsigned)v.grid, 1, 1, (unsigned)v.block, 1, 1, (unsigned)v.smem, stream,
+    CU_CHECK(cuda().cuLaunchKernel(fn, (unsigned)v.grid, (unsigned)v.grid_y, (unsigned)v.grid_z, (unsigned)v.block, 1, 1, (unsigned)v.smem, stream,
                                    args.data(), nullptr));
   }
 }

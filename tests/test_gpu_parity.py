@@ -176,3 +176,61 @@ def test_misc_memory_bound_ops(ctx):
     for i in gen[:: max(1, len(gen) // 40)]:
         c.check(c.completion([i]))
     c.check(c.kg.operator_aligned())
+
+
+@pytest.mark.gpu
+def test_c2_every_gemm_candidate(ctx):
+    """Every tcgen05 GEMM candidate of the ViT attention layer (fused views + epilogues)."""
+    c = Case(ctx, c2_vit_attention())
+    gem = [x["index"] for x in c.cands if x["klass"] == "gemm"]
+    assert len(gem) > 30
+    for i in gem:
+        c.check(c.completion([i]))
+
+
+@pytest.mark.gpu
+def test_c2_memory_bound_candidates(ctx):
+    c = Case(ctx, c2_vit_attention())
+    mb = [x["index"] for x in c.cands if x["klass"] in ("pw", "rr")]
+    for i in mb:
+        c.check(c.completion([i]))
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("kw", [dict(), dict(batch=2, seq=64, hidden=256, heads=4), dict(seq=200, hidden=192, heads=3)])
+def test_c2_pipeline(ctx, kw):
+    """profile -> BLP -> execute for several attention shapes (batched, M tails)."""
+    c = Case(ctx, c2_vit_attention(**kw))
+    costs = c.kg.profile()
+    obj, sel = c.kg.select(costs)
+    base = c.kg.operator_aligned()
+    assert obj <= sum(costs[i] for i in base)
+    c.check(sel)
+    c.check(base)
+    c.check(c.kg.singletons())
+
+
+def _gemm_graph(m, k, n, batch=1, act="Relu"):
+    b = GraphBuilder("bf16")
+    x = b.input("x", [batch, m, k])
+    w = b.input("w", [k, n], std=k ** -0.5)
+    bias = b.input("bias", [n], std=0.1)
+    r = b.input("r", [batch, m, n])
+    y = b.op("MatMul", x, w)
+    y = b.op("Add", y, bias)
+    y = b.op(act, y)
+    y = b.op("Add", y, r)
+    b.output(y)
+    return b.build()
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("m,k,n,batch", [(128, 64, 64, 1), (200, 96, 104, 1), (300, 320, 384, 2), (64, 16, 48, 3),
+                                         (1024, 768, 2304, 1)])
+def test_gemm_shapes(ctx, m, k, n, batch):
+    """Ragged M (row mask), K (TMA zero fill), N (column mask), multi-tile grids, every
+    generable candidate (GEMM with 0..3 fused epilogue primitives)."""
+    c = Case(ctx, _gemm_graph(m, k, n, batch))
+    for x in c.cands:
+        if x["klass"] != "rejected":
+            c.check(c.completion([x["index"]]))
