@@ -64,7 +64,7 @@ class Clocks:
                  "--query-gpu=clocks.sm,clocks.max.sm,clocks_event_reasons.active,"
                  "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
                  "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap",
-                 "--format=csv,noheader,nounits", "-lms", "100"],
+                 "--format=csv,noheader,nounits", "-lms", "50"],
                 stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
         except Exception:
             self.proc = None
@@ -181,6 +181,7 @@ def main():
     ap.add_argument("--impl", default="korch", choices=["korch", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-budget", type=float, default=15.0)
+    ap.add_argument("--save-selection", default=None, help="write the chosen plan (for tools/replay.py)")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
     if args.impl == "reference":
@@ -221,6 +222,12 @@ def main():
     base_obj = sum(costs[i] for i in base) if all(costs[i] < K.INF for i in base) else None
     kg.set_orchestration(sel)
     order = kg.plan()
+    if args.save_selection:
+        json.dump({"config": args.config, "batch": 1, "selection": sel,
+                   "variants": {str(i): kg.variant_info(i)[1] for i in order},
+                   "tags": {str(i): kg.variant_info(i)[2] for i in order},
+                   "kernels": {str(i): cands[i]["signature"] for i in order},
+                   "costs_ns": {str(i): costs[i] for i in order}}, open(args.save_selection, "w"), indent=1)
     tuning = {"enumerate_s": t_enum, "compile_s": t_compile, "profile_s": t_prof, "select_s": t_sel,
               "total_s": time.perf_counter() - t_all, "n_candidates": len(cands), "n_states": kg.n_states,
               "n_generable": len(kg.generable()), "n_prims": kg.n_prims}
@@ -245,12 +252,24 @@ def main():
         dist.barrier()
     torch.cuda.synchronize()
     with Clocks(local) as clk:
+        # keep the GPU busy with the same workload until the sampler has produced samples,
+        # then run the timed steps (each bracketed by events, L2 flushed in between)
+        t_start = time.perf_counter()
+        while time.perf_counter() - t_start < 0.6:
+            for _ in range(50):
+                step()
+            torch.cuda.synchronize()
         for i in range(args.steps):
             flush.fill_(i & 0xFF)
             ev[i][0].record(stream)
             step()
             ev[i][1].record(stream)
         torch.cuda.synchronize()
+        t_end = time.perf_counter()
+        while time.perf_counter() - t_end < 0.3:
+            for _ in range(50):
+                step()
+            torch.cuda.synchronize()
     if world > 1:
         dist.barrier()
     times = [a.elapsed_time(b) for a, b in ev]

@@ -154,6 +154,17 @@ korch_status korch_compile(korch_graph* g, const int64_t* idx, int64_t n, int32_
 korch_status korch_profile(korch_graph* g, const int64_t* idx, int64_t n,
                            const korch_prof_opts* opts, int64_t* cost_ns);
 
+/* Launch variants of candidate i (tile / thread-group configurations of its
+ * template; the profiler keeps the fastest).  *n_variants and *chosen (-1 = not
+ * profiled yet, variant 0 is used) may be NULL; tag receives the chosen (or
+ * first) variant's description, same buffer protocol as korch_graph_dump. */
+korch_status korch_variant_info(const korch_graph* g, int64_t i, int32_t* n_variants, int32_t* chosen,
+                                char* tag, size_t cap);
+
+/* Force candidate i to use launch variant v (e.g. to replay a plan without
+ * re-profiling).  Takes effect at the next korch_set_orchestration. */
+korch_status korch_select_variant(korch_graph* g, int64_t i, int32_t v);
+
 /* Accept a selection u (sel[0..n) candidate indices with u_i = 1).  Checks Eq. 3
  * and Eq. 4 (KORCH_E_INFEASIBLE), that no member was rejected
  * (KORCH_E_NOT_SCHEDULABLE); orders kernels by the topological index of their

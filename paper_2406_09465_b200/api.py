@@ -151,7 +151,20 @@ class KorchGraph:
     def singletons(self):
         return singletons(self.cands, self.n_prims)
 
-    def set_orchestration(self, sel) -> int:
+    def variant_info(self, i: int):
+        """(number of launch variants, chosen variant or -1, tag of the chosen/first one)."""
+        nv, ch = C.c_int32(), C.c_int32()
+        buf = C.create_string_buffer(512)
+        check(LIB.korch_variant_info(self.h, i, C.byref(nv), C.byref(ch), buf, len(buf)))
+        return nv.value, ch.value, buf.value.decode()
+
+    def set_variant(self, i: int, v: int):
+        check(LIB.korch_select_variant(self.h, i, v))
+
+    def set_orchestration(self, sel, variants=None) -> int:
+        """Accept selection `sel`; `variants` ({cand: variant}) pins launch variants."""
+        for i, v in (variants or {}).items():
+            self.set_variant(int(i), int(v))
         arr = _lib.i64_array(list(sel))
         ws = C.c_size_t()
         check(LIB.korch_set_orchestration(self.h, arr, len(sel), C.byref(ws)))

@@ -598,6 +598,31 @@ korch_status korch_profile(korch_graph* G, const int64_t* idx, int64_t n, const 
   })
 }
 
+korch_status korch_variant_info(const korch_graph* G, int64_t i, int32_t* nv, int32_t* chosen, char* tag,
+                                size_t cap) {
+  if (!G) return fail(KORCH_E_ARG, "NULL graph");
+  if (i < 0 || i >= (int64_t)G->cands.size()) return fail(KORCH_E_ARG, "candidate index out of range");
+  const CandState& s = G->cs[i];
+  if (nv) *nv = (int32_t)s.plan.variants.size();
+  if (chosen) *chosen = s.best;
+  if (tag && cap) {
+    std::string t = s.plan.variants.empty() ? "rejected: " + s.plan.reject
+                                            : s.plan.variants[s.best >= 0 ? s.best : 0].tag;
+    size_t need;
+    return write_buf(t, tag, cap, &need);
+  }
+  return KORCH_OK;
+}
+
+korch_status korch_select_variant(korch_graph* G, int64_t i, int32_t v) {
+  if (!G) return fail(KORCH_E_ARG, "NULL graph");
+  if (i < 0 || i >= (int64_t)G->cands.size()) return fail(KORCH_E_ARG, "candidate index out of range");
+  CandState& s = G->cs[i];
+  if (v < 0 || v >= (int32_t)s.plan.variants.size()) return fail(KORCH_E_ARG, "variant index out of range");
+  s.best = v;
+  return KORCH_OK;
+}
+
 korch_status korch_set_orchestration(korch_graph* G, const int64_t* sel, int64_t n, size_t* ws) {
   if (!G || (n > 0 && !sel)) return fail(KORCH_E_ARG, "NULL argument");
   KORCH_TRY({
@@ -735,13 +760,22 @@ korch_status korch_execute(korch_graph* G, const void* const* inputs, void* cons
     for (size_t i = 0; i < g.inputs.size(); ++i) ptrs.push_back(inputs[i]);
     for (size_t i = 0; i < g.outputs.size(); ++i) ptrs.push_back(outputs[i]);
     ptrs.push_back(workspace);
+    auto resolve = [&](const BufRef& b) -> void* {
+      if (b.kind == BufRef::Input) return const_cast<void*>(inputs[b.index]);
+      if (b.kind == BufRef::Output) return outputs[b.index];
+      return static_cast<char*>(workspace) + b.offset;
+    };
+    static const bool direct = getenv("KORCH_EXEC_DIRECT") != nullptr;
+    if (direct) {  // plain stream launches (profilers that cannot follow graph replays)
+      for (auto& st : G->steps) {
+        std::vector<const void*> ins;
+        for (auto& a : st.args) ins.push_back(resolve(a));
+        launch_variant(ctx, G->cs[st.cand].plan, st.variant, ins, resolve(st.out), (CUstream)stream);
+      }
+      return KORCH_OK;
+    }
     if (!G->gexec || ptrs != G->cap_ptrs) {
       if (G->gexec) { cu.cuGraphExecDestroy(G->gexec); G->gexec = nullptr; }
-      auto resolve = [&](const BufRef& b) -> void* {
-        if (b.kind == BufRef::Input) return const_cast<void*>(inputs[b.index]);
-        if (b.kind == BufRef::Output) return outputs[b.index];
-        return static_cast<char*>(workspace) + b.offset;
-      };
       CU_CHECK(cu.cuStreamBeginCapture(ctx->pstream, CU_STREAM_CAPTURE_MODE_THREAD_LOCAL));
       try {
         for (auto& st : G->steps) {
