@@ -55,7 +55,7 @@ struct GemmEpilogue {
   int64_t bytes = 0;                  // epilogue reads + output write
   std::vector<std::string> batch_vars;
 };
-bool make_gemm_epilogue(const Graph& g, const Candidate& c, int mm, const std::vector<Ref>& pre_ext,
+bool make_gemm_epilogue(const Graph& g, const Candidate& c, int mm, int cw, const std::vector<Ref>& pre_ext,
                         GemmEpilogue* out, std::string* err);
 KernelPlan generate_gemm(const Graph& g, const Candidate& c);   // gemm_gen.cpp
 std::string kernel_prelude();

@@ -189,9 +189,16 @@ KernelPlan generate_gemm(const Graph& g, const Candidate& c) {
     return true;
   };
 
+  bool has_reduce = false;
+  for (int m : c.members)
+    if (g.prims[m].kind == Kind::Reduce) has_reduce = true;
+  if (has_reduce && (N % 32 || N > 256)) {
+    kp.reject = "in-tile row reduction needs N % 32 == 0 and N <= 256";
+    return kp;
+  }
   std::vector<Ref> pre{va.src, vb.src};
   GemmEpilogue ep;
-  if (!make_gemm_epilogue(g, c, mm, pre, &ep, &err)) {
+  if (!make_gemm_epilogue(g, c, mm, has_reduce ? (int)N : 32, pre, &ep, &err)) {
     kp.reject = err;
     return kp;
   }
@@ -203,20 +210,38 @@ KernelPlan generate_gemm(const Graph& g, const Candidate& c) {
   int64_t a_el = numel(va.shape), b_el = numel(vb.shape);
   kp.bytes = ep.bytes + 2 * (a_el + b_el);
 
+  // Tile widths: small BN spreads a skinny (small-M, weight-streaming) GEMM over more
+  // SMs; large BN maximises operand reuse.  The profiler keeps the fastest.
   std::vector<int> bns;
-  for (int bn : {64, 128, 256})
-    if (bn <= 64 || bn / 2 < N) bns.push_back(bn);
+  if (has_reduce) {
+    // in-tile row reduction: one tile spans the whole row, each thread owns a row
+    bns.push_back((int)N);
+  } else {
+    for (int bn : {16, 32, 64, 128, 256})
+      if (bn <= 64 || bn / 2 < N) bns.push_back(bn);
+  }
   for (int BN : bns) {
+    // epilogue chunk (TMEM columns per pass); the whole row when reducing
+    const int CW = has_reduce ? BN : (BN < 32 ? BN : 32);
+    GemmEpilogue epv;
+    if (!make_gemm_epilogue(g, c, mm, CW, pre, &epv, &err)) continue;
     TmaDesc da, db;
     std::vector<int> ba_axes, bb_axes;
+    // MN-major B narrower than a 128B swizzle atom uses the 64B / 32B swizzle modes
+    const int bmn_box = BN < 64 ? BN : 64;
+    const int b_swz_tma = bmn_box == 64 ? 3 : bmn_box == 32 ? 2 : 1;       // CUtensorMapSwizzle
+    const int b_swz_umma = bmn_box == 64 ? 2 : bmn_box == 32 ? 4 : 6;      // UMMA layout type
+    const int b_row_bytes = bmn_box * 2;                                    // one K row of a B atom
     bool ok = a_kmaj ? build_desc(va, slotA, K, M, a_m, 64, 128, nbA, &ba_axes, &da)
                      : build_desc(va, slotA, M, K, a_k, 64, 64, nbA, &ba_axes, &da);
     ok = ok && (b_kmaj ? build_desc(vb, slotB, K, N, b_n, 64, (uint32_t)BN, nbB, &bb_axes, &db)
-                       : build_desc(vb, slotB, N, K, b_k, 64, 64, nbB, &bb_axes, &db));
+                       : build_desc(vb, slotB, N, K, b_k, (uint32_t)bmn_box, 64, nbB, &bb_axes, &db));
     if (!ok) {
       kp.reject = "operand strides not expressible as a TMA tensor map";
       continue;
     }
+    if (!b_kmaj) db.swizzle = b_swz_tma;
+    const GemmEpilogue& ep = epv;
     const int S = 4;
     const int A_BYTES = 128 * 64 * 2, B_BYTES = BN * 64 * 2, STAGE = A_BYTES + B_BYTES;
     const int smem = S * STAGE + 1024 + (2 * S + 1) * 8 + 16;
@@ -256,6 +281,7 @@ KernelPlan generate_gemm(const Graph& g, const Candidate& c) {
     k << "  if (warp == 2) tc_alloc(tslot, " << tcols << ");\n";
     k << "  tc_fence_before();\n  __syncthreads();\n  tc_fence_after();\n";
     k << "  const unsigned tmem = *tslot;\n";
+    k << "  pdl_trigger();\n  pdl_wait();\n";
     // producer
     k << "  if (warp == 0 && lane == 0) {\n";
     k << "    int s = 0; unsigned ph = 0;\n";
@@ -274,7 +300,7 @@ KernelPlan generate_gemm(const Graph& g, const Candidate& c) {
     if (b_kmaj) {
       k << "      " << load(db.rank) << "(sb, &tmB, full + s, " << coords("kb * 64", "tile_n", bb_axes) << ");\n";
     } else {
-      for (int cc = 0; cc < BN / 64; ++cc)
+      for (int cc = 0; cc < (BN + 63) / 64; ++cc)
         k << "      " << load(db.rank) << "(sb + " << cc * 8192 << ", &tmB, full + s, "
           << coords("tile_n + " + str(cc * 64), "kb * 64", bb_axes) << ");\n";
     }
@@ -288,8 +314,11 @@ KernelPlan generate_gemm(const Graph& g, const Candidate& c) {
     k << "      #pragma unroll\n      for (int k = 0; k < 4; ++k) {\n";
     k << "        const unsigned long long ad = umma_desc(sa + " << (a_kmaj ? "k * 32" : "k * 2048") << ", "
       << (a_kmaj ? 16 : 8192) << ", 1024);\n";
-    k << "        const unsigned long long bd = umma_desc(sb + " << (b_kmaj ? "k * 32" : "k * 2048") << ", "
-      << (b_kmaj ? 16 : 8192) << ", 1024);\n";
+    if (b_kmaj)
+      k << "        const unsigned long long bd = umma_desc(sb + k * 32, 16, 1024);\n";
+    else
+      k << "        const unsigned long long bd = umma_desc(sb + k * " << 16 * b_row_bytes << ", 8192, "
+        << 8 * b_row_bytes << ", " << b_swz_umma << ");\n";
     k << "        tc_mma(tmem, ad, bd, " << idesc << "u, (kb | k) != 0);\n      }\n";
     k << "      tc_commit(empty + s);\n";
     k << "      if (++s == " << S << ") { s = 0; ph ^= 1u; }\n    }\n";
@@ -297,10 +326,15 @@ KernelPlan generate_gemm(const Graph& g, const Candidate& c) {
     // epilogue
     k << "  __syncwarp();\n  mbar_wait(accf, 0);\n  __syncwarp();\n  tc_fence_after();\n";
     k << "  {\n    const int gm = tile_m + warp * 32 + lane;\n    const int tid = 0;\n    (void)tid;\n";
-    k << "    #pragma unroll 1\n    for (int ch = 0; ch < " << BN / 32 << "; ++ch) {\n";
-    k << "      const int nb = tile_n + ch * 32;\n";
-    k << "      float acc[32];\n";
-    k << "      tc_ld32(tmem + ((unsigned)(warp * 32) << 16) + (unsigned)(ch * 32), acc);\n";
+    k << "    #pragma unroll 1\n    for (int ch = 0; ch < " << BN / CW << "; ++ch) {\n";
+    k << "      const int nb = tile_n + ch * " << CW << ";\n";
+    k << "      float acc[" << CW << "];\n";
+    if (CW <= 32) {
+      k << "      tc_ld" << CW << "(tmem + ((unsigned)(warp * 32) << 16) + (unsigned)(ch * " << CW << "), acc);\n";
+    } else {
+      k << "      #pragma unroll\n      for (int q = 0; q < " << CW / 32 << "; ++q)\n"
+        << "        tc_ld32(tmem + ((unsigned)(warp * 32) << 16) + (unsigned)(ch * " << CW << " + q * 32), acc + q * 32);\n";
+    }
     k << "      if (gm < " << M << " && nb < " << N << ") {\n";
     k << ep.body << ep.store;
     k << "      }\n    }\n  }\n";

@@ -278,7 +278,7 @@ static void encode_tma(const TmaDesc& d, const void* base, CUtensorMap* out) {
 }
 
 static void launch_variant(korch_ctx* ctx, const KernelPlan& plan, int vi, const std::vector<const void*>& ins,
-                           void* out, CUstream stream) {
+                           void* out, CUstream stream, bool pdl = false) {
   const KernelVariant& v = plan.variants[vi];
   Module* m = ctx->module_for(v.name);
   CUfunction fn = load_fn(ctx, m, v);
@@ -298,7 +298,7 @@ static void launch_variant(korch_ctx* ctx, const KernelPlan& plan, int vi, const
     encode_tma(d, base, &maps[t]);
     args.push_back(&maps[t]);
   }
-  if (v.cluster > 1) {
+  if (v.cluster > 1 || pdl) {
     CUlaunchConfig cfg{};
     cfg.gridDimX = (unsigned)v.grid;
     cfg.gridDimY = (unsigned)v.grid_y;
@@ -307,12 +307,21 @@ static void launch_variant(korch_ctx* ctx, const KernelPlan& plan, int vi, const
     cfg.blockDimY = cfg.blockDimZ = 1;
     cfg.sharedMemBytes = (unsigned)v.smem;
     cfg.hStream = stream;
-    CUlaunchAttribute at;
-    at.id = CU_LAUNCH_ATTRIBUTE_CLUSTER_DIMENSION;
-    at.value.clusterDim.x = (unsigned)v.cluster;
-    at.value.clusterDim.y = at.value.clusterDim.z = 1;
-    cfg.attrs = &at;
-    cfg.numAttrs = 1;
+    CUlaunchAttribute at[2];
+    unsigned na = 0;
+    if (v.cluster > 1) {
+      at[na].id = CU_LAUNCH_ATTRIBUTE_CLUSTER_DIMENSION;
+      at[na].value.clusterDim.x = (unsigned)v.cluster;
+      at[na].value.clusterDim.y = at[na].value.clusterDim.z = 1;
+      ++na;
+    }
+    if (pdl) {  // programmatic dependent launch (the kernel calls griddepcontrol.wait)
+      at[na].id = CU_LAUNCH_ATTRIBUTE_PROGRAMMATIC_STREAM_SERIALIZATION;
+      at[na].value.programmaticStreamSerializationAllowed = 1;
+      ++na;
+    }
+    cfg.attrs = at;
+    cfg.numAttrs = na;
     CU_CHECK(cuda().cuLaunchKernelEx(&cfg, fn, args.data(), nullptr));
   } else {
     CU_CHECK(cuda().cuLaunchKernel(fn, (unsigned)v.grid, (unsigned)v.grid_y, (unsigned)v.grid_z, (unsigned)v.block, 1, 1, (unsigned)v.smem, stream,
@@ -766,6 +775,7 @@ korch_status korch_execute(korch_graph* G, const void* const* inputs, void* cons
       return static_cast<char*>(workspace) + b.offset;
     };
     static const bool direct = getenv("KORCH_EXEC_DIRECT") != nullptr;
+    static const bool use_pdl = !(getenv("KORCH_PDL") && std::string(getenv("KORCH_PDL")) == "0");
     if (direct) {  // plain stream launches (profilers that cannot follow graph replays)
       for (auto& st : G->steps) {
         std::vector<const void*> ins;
@@ -778,10 +788,12 @@ korch_status korch_execute(korch_graph* G, const void* const* inputs, void* cons
       if (G->gexec) { cu.cuGraphExecDestroy(G->gexec); G->gexec = nullptr; }
       CU_CHECK(cu.cuStreamBeginCapture(ctx->pstream, CU_STREAM_CAPTURE_MODE_THREAD_LOCAL));
       try {
-        for (auto& st : G->steps) {
+        for (size_t k = 0; k < G->steps.size(); ++k) {
+          const Step& st = G->steps[k];
           std::vector<const void*> ins;
           for (auto& a : st.args) ins.push_back(resolve(a));
-          launch_variant(ctx, G->cs[st.cand].plan, st.variant, ins, resolve(st.out), ctx->pstream);
+          // every kernel after the first overlaps its prologue with its predecessor (PDL)
+          launch_variant(ctx, G->cs[st.cand].plan, st.variant, ins, resolve(st.out), ctx->pstream, use_pdl && k > 0);
         }
       } catch (...) {
         CUgraph tmp = nullptr;

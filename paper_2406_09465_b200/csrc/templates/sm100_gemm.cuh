@@ -73,14 +73,16 @@ static __device__ __forceinline__ void tma_load_5d(void* dst, const TmaMap* m, u
 }
 
 // ---------------------------------------------------------------- tcgen05
-// Shared-memory matrix descriptor (SWIZZLE_128B, Blackwell version bits = 1).
-static __device__ __forceinline__ unsigned long long umma_desc(unsigned saddr, unsigned lbo, unsigned sbo) {
+// Shared-memory matrix descriptor (Blackwell version bits = 1).  layout: 2 = SWIZZLE_128B,
+// 4 = SWIZZLE_64B, 6 = SWIZZLE_32B (bits 61-63).
+static __device__ __forceinline__ unsigned long long umma_desc(unsigned saddr, unsigned lbo, unsigned sbo,
+                                                               unsigned layout = 2) {
   unsigned long long d = 0;
   d |= (unsigned long long)((saddr >> 4) & 0x3FFF);
   d |= (unsigned long long)((lbo >> 4) & 0x3FFF) << 16;
   d |= (unsigned long long)((sbo >> 4) & 0x3FFF) << 32;
   d |= 1ull << 46;                  // version = 1 (sm_100)
-  d |= 2ull << 61;                  // layout = SWIZZLE_128B
+  d |= (unsigned long long)layout << 61;
   return d;
 }
 static __device__ __forceinline__ void tc_alloc(unsigned* dst_smem, unsigned ncols) {
@@ -121,6 +123,19 @@ static __device__ __forceinline__ void tc_ld32(unsigned taddr, float* v) {
   asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
 #pragma unroll
   for (int i = 0; i < 32; ++i) v[i] = __uint_as_float(r[i]);
+}
+// 32 lanes x 16 columns (BN = 16 tiles).
+static __device__ __forceinline__ void tc_ld16(unsigned taddr, float* v) {
+  unsigned r[16];
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x16.b32 "
+      "{%0, %1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, %12, %13, %14, %15}, [%16];"
+      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]), "=r"(r[8]),
+        "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15])
+      : "r"(taddr));
+  asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+#pragma unroll
+  for (int i = 0; i < 16; ++i) v[i] = __uint_as_float(r[i]);
 }
 static __device__ __forceinline__ bool elect_one() {
   unsigned pred = 0;
