@@ -227,7 +227,10 @@ def main():
                    "variants": {str(i): kg.variant_info(i)[1] for i in order},
                    "tags": {str(i): kg.variant_info(i)[2] for i in order},
                    "kernels": {str(i): cands[i]["signature"] for i in order},
-                   "costs_ns": {str(i): costs[i] for i in order}}, open(args.save_selection, "w"), indent=1)
+                   "costs_ns": {str(i): costs[i] for i in order},
+                   "all_costs_ns": costs,
+                   "all_variants": [kg.variant_info(i)[1] for i in range(len(cands))]},
+                  open(args.save_selection, "w"), indent=1)
     tuning = {"enumerate_s": t_enum, "compile_s": t_compile, "profile_s": t_prof, "select_s": t_sel,
               "total_s": time.perf_counter() - t_all, "n_candidates": len(cands), "n_states": kg.n_states,
               "n_generable": len(kg.generable()), "n_prims": kg.n_prims}

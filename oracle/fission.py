@@ -39,6 +39,7 @@ class _PG:
         self.dtype = graph["dtype"]
         self.in_shapes = {s["name"]: tuple(s["shape"]) for s in graph["inputs"]}
         self.nodes = []
+        self.op = None
 
     def shape(self, ref):
         return self.in_shapes[ref[1]] if ref[0] == "input" else self.nodes[ref[1]]["shape"]
@@ -47,7 +48,7 @@ class _PG:
         shp = infer_shape(kind, attrs, [self.shape(r) for r in inputs])
         nid = len(self.nodes)
         self.nodes.append({"id": nid, "kind": kind, "attrs": attrs, "inputs": list(inputs),
-                           "shape": tuple(shp)})
+                           "shape": tuple(shp), "op": self.op})
         return ("node", nid)
 
 
@@ -98,6 +99,7 @@ def fission(graph: dict) -> dict:
     out_of = {}
     for oid in order:
         op = ops[oid]
+        pg.op = oid
         ins = [("node", out_of[r["node"]]) if "node" in r else ("input", r["input"])
                for r in op["inputs"]]
         k, at = op["kind"], dict(op["attrs"])
@@ -157,11 +159,16 @@ def fission(graph: dict) -> dict:
         else:
             raise NotImplementedError(f"no fission rule for {k}")
         out_of[oid] = ref[1]
-    return {"version": 1, "level": "primitive", "dtype": graph["dtype"],
-            "inputs": [dict(s) for s in graph["inputs"]],
-            "nodes": pg.nodes,
-            "outputs": [out_of[o] for o in graph["outputs"]],
-            "op_of": _op_membership(pg, order, out_of)}
+    res = {"version": 1, "level": "primitive", "dtype": graph["dtype"],
+           "inputs": [dict(s) for s in graph["inputs"]],
+           "nodes": pg.nodes,
+           "outputs": [out_of[o] for o in graph["outputs"]],
+           "op_of": _op_membership(pg, order, out_of)}
+    if graph.get("rewrites"):
+        # R1-R3, applied after fission when the graph asks for them
+        from .rewrites import apply_r1_r3
+        res = apply_r1_r3(res)
+    return res
 
 
 def _op_membership(pg, order, out_of):

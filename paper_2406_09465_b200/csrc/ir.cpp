@@ -440,6 +440,7 @@ Graph fission_graph(const Json& j) {
     out_of[oid] = res.id;
   }
   for (auto& o : j["outputs"].arr) g.outputs.push_back(out_of.at(o.as_int()));
+  if (j.has("rewrites") && j["rewrites"].type == Json::Bool && j["rewrites"].b) apply_r1_r3(g);
   return g;
 }
 

@@ -112,5 +112,7 @@ Graph load_graph(const char* json, size_t n);
 std::string dump_graph(const Graph& g);
 std::string validate_graph(const Graph& g);
 Shape infer_shape(const Graph& g, const Prim& p);
+// R1-R3 at every Softmax -> MatMul site (rewrites.cpp); renumbers primitives.
+void apply_r1_r3(Graph& g);
 
 }  // namespace korch

@@ -197,10 +197,17 @@ def test_c2_memory_bound_candidates(ctx):
 
 
 @pytest.mark.gpu
-@pytest.mark.parametrize("kw", [dict(), dict(batch=2, seq=64, hidden=256, heads=4), dict(seq=200, hidden=192, heads=3)])
+@pytest.mark.parametrize("kw", [dict(), dict(batch=2, seq=64, hidden=256, heads=4), dict(seq=200, hidden=192, heads=3),
+                                dict(rewrites=True), dict(batch=2, seq=64, hidden=256, heads=4, rewrites=True)])
 def test_c2_pipeline(ctx, kw):
-    """profile -> BLP -> execute for several attention shapes (batched, M tails)."""
-    c = Case(ctx, c2_vit_attention(**kw))
+    """profile -> BLP -> execute for several attention shapes (batched, M tails), with and
+    without the R1-R3 rewrites."""
+    kw = dict(kw)
+    rw = kw.pop("rewrites", False)
+    g = c2_vit_attention(**kw)
+    if rw:
+        g["rewrites"] = True
+    c = Case(ctx, g)
     costs = c.kg.profile()
     obj, sel = c.kg.select(costs)
     base = c.kg.operator_aligned()

@@ -57,6 +57,15 @@ def _misc_graph():
 GRAPHS["misc"] = _misc_graph
 
 
+def _rw(g):
+    g["rewrites"] = True
+    return g
+
+
+GRAPHS["c2_r1r3"] = lambda: _rw(c2_vit_attention())
+GRAPHS["c2_b2_r1r3"] = lambda: _rw(c2_vit_attention(batch=2, seq=32, hidden=128, heads=4))
+
+
 @pytest.mark.parametrize("name", sorted(GRAPHS))
 def test_fission_matches_oracle(ctx, name):
     g = GRAPHS[name]()
