@@ -141,6 +141,50 @@ def oracle_baseline(graph, sel_cands, sel, budget_s=15.0):
             "sample": f"{n} inferences of the selected orchestration (fp64 numpy, bf16/fp32 rounding at kernel outputs), {el:.1f} s"}
 
 
+def bandwidth_variant(K, pk, steps=10):
+    """C1 at x[2^20,128] fp32 (SURVEY.md §8(d) C1 bandwidth variant): enumerate, profile
+    (cold, inputs > L2), BLP-select, execute; achieved GB/s of the plan and of its
+    dominant kernel against the measured HBM peak."""
+    import torch
+    graph, cfg = config_graph("c1_bw")
+    ctx = K.Context(torch.cuda.current_device())
+    kg = K.KorchGraph(ctx, graph)
+    cands = kg.enumerate()
+    costs = kg.profile(warmup=1, launches=2, trials=3)
+    obj, sel = kg.select(costs)
+    kg.set_orchestration(sel)
+    order = kg.plan()
+    x = torch.randn(graph["inputs"][0]["shape"], device="cuda")
+    g = 1 + 0.1 * torch.randn(graph["inputs"][1]["shape"], device="cuda")
+    b = 0.1 * torch.randn(graph["inputs"][2]["shape"], device="cuda")
+    outs, ws = kg.torch_outputs(), kg.torch_workspace()
+    stream = torch.cuda.current_stream()
+    for _ in range(2):
+        kg.execute([x, g, b], outs, ws, stream)
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(steps)]
+    torch.cuda.synchronize()
+    for a, e in ev:
+        a.record(stream)
+        kg.execute([x, g, b], outs, ws, stream)
+        e.record(stream)
+    torch.cuda.synchronize()
+    ms = statistics.median(a.elapsed_time(e) for a, e in ev)
+    plan_bytes = sum(cands[i]["bytes"] for i in order)
+    dom = max(order, key=lambda i: costs[i])
+    res = {"workload": cfg["workload"], "kernels": len(order), "ms": ms, "plan_bytes": plan_bytes,
+           "achieved_gbs": plan_bytes / (ms * 1e-3) / 1e9, "peak_gbs": pk["hbm_gbs"],
+           "frac": plan_bytes / (ms * 1e-3) / 1e9 / pk["hbm_gbs"],
+           "dominant": {"candidate": dom, "members": len(cands[dom]["members"]), "class": cands[dom]["klass"],
+                        "bytes": cands[dom]["bytes"], "ns": costs[dom],
+                        "gbs": cands[dom]["bytes"] / costs[dom], "variant": kg.variant_info(dom)[2],
+                        "name": cands[dom]["signature"]},
+           "blp_objective_ns": obj,
+           "operator_aligned_ns": sum(costs[i] for i in kg.operator_aligned())}
+    del x, outs, ws
+    ctx.close()
+    return res
+
+
 def run_reference(args):
     """--impl reference: the oracle (the paper has no runnable reference here), timed on the
     host cores on this arm's workload, bounded to a few minutes."""
@@ -180,6 +224,7 @@ def main():
     ap.add_argument("--config", default=os.environ.get("KORCH_BENCH_CONFIG", "c2"))
     ap.add_argument("--impl", default="korch", choices=["korch", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-bw-variant", action="store_true", help="skip the C1 x[2^20,128] bandwidth measurement")
     ap.add_argument("--cpu-budget", type=float, default=15.0)
     ap.add_argument("--save-selection", default=None, help="write the chosen plan (for tools/replay.py)")
     args = ap.parse_args()
@@ -337,15 +382,16 @@ def main():
                       "algorithmic_bytes": dc["bytes"], "flops": dc["flops"], "ns_cold_l2": dom_cold,
                       "ns_warm": costs[dom], "name": dc["signature"], "peak_source": pk["source"]}
 
-    # gather max over ranks
-    ms_max, e2e_max = ms, e2e_ms
-    if world > 1:
-        t = torch.tensor([ms, e2e_ms], device="cuda", dtype=torch.float64)
-        allt = [torch.zeros_like(t) for _ in range(world)]
-        dist.all_gather(allt, t)
-        ms_max = max(float(x[0]) for x in allt)
-        e2e_max = max(float(x[1]) for x in allt)
+    # gather max over ranks (G4): a step takes as long as its slowest rank
+    from paper_2406_09465_b200.dist import max_over_ranks
+    ms_max, e2e_max = max_over_ranks([ms, e2e_ms], device="cuda")
 
+    bw = None
+    if rank == 0 and world == 1 and not args.no_bw_variant:
+        try:
+            bw = bandwidth_variant(K, pk)
+        except Exception as e:  # reported, never silently replaced
+            bw = {"error": str(e)[:300]}
     if rank == 0:
         cpu = None
         if not args.no_cpu_baseline and world == 1:
@@ -364,6 +410,7 @@ def main():
             "selection": {"blp_objective_ns": obj, "operator_aligned_ns": base_obj,
                           "operator_aligned_kernels": len(base), "kernels": order},
             "roofline": roof,
+            "bandwidth_variant": bw,
             "cpu_baseline": cpu,
             "clocks": clk.summary(),
             "tuning": tuning,

@@ -8,6 +8,7 @@
 // (kernel k5) without materialising the transposed operand.  Downstream members
 // (elementwise ops, port broadcasts, side-branch reads, Transpose/Reshape of the result)
 // are fused into the epilogue, emitted by the row-template machinery.
+#include <algorithm>
 #include <set>
 #include <sstream>
 
@@ -242,10 +243,12 @@ KernelPlan generate_gemm(const Graph& g, const Candidate& c) {
     }
     if (!b_kmaj) db.swizzle = b_swz_tma;
     const GemmEpilogue& ep = epv;
-    const int S = 4;
     const int A_BYTES = 128 * 64 * 2, B_BYTES = BN * 64 * 2, STAGE = A_BYTES + B_BYTES;
-    const int smem = S * STAGE + 1024 + (2 * S + 1) * 8 + 16;
     const int64_t NK = (K + 63) / 64;
+    // Pipeline depth: keep as many K-blocks in flight as shared memory allows (up to all
+    // of them) -- small-M GEMMs are bound by TMA round-trip latency, not bandwidth.
+    const int S = (int)std::max<int64_t>(2, std::min<int64_t>(NK, (200 * 1024) / STAGE));
+    const int smem = S * STAGE + 1024 + (2 * S + 1) * 8 + 16;
     const int tcols = BN < 32 ? 32 : BN;
     uint32_t idesc = (1u << 4) | (1u << 7) | (1u << 10) | ((a_kmaj ? 0u : 1u) << 15) | ((b_kmaj ? 0u : 1u) << 16) |
                      ((uint32_t)(BN >> 3) << 17) | ((uint32_t)(128 >> 4) << 24);
