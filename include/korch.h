@@ -161,6 +161,10 @@ korch_status korch_profile(korch_graph* g, const int64_t* idx, int64_t n,
 korch_status korch_variant_info(const korch_graph* g, int64_t i, int32_t* n_variants, int32_t* chosen,
                                 char* tag, size_t cap);
 
+/* Profiled median time of launch variant v of candidate i in integer ns (-1 if it
+ * was not profiled, INT64_MAX if it failed to launch). */
+korch_status korch_variant_cost(const korch_graph* g, int64_t i, int32_t v, int64_t* ns);
+
 /* Force candidate i to use launch variant v (e.g. to replay a plan without
  * re-profiling).  Takes effect at the next korch_set_orchestration. */
 korch_status korch_select_variant(korch_graph* g, int64_t i, int32_t v);

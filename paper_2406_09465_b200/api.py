@@ -158,6 +158,16 @@ class KorchGraph:
         check(LIB.korch_variant_info(self.h, i, C.byref(nv), C.byref(ch), buf, len(buf)))
         return nv.value, ch.value, buf.value.decode()
 
+    def variant_costs(self, i: int):
+        """[(tag, ns)] for every launch variant of candidate i (ns = -1 if not profiled)."""
+        nv, _, _ = self.variant_info(i)
+        out = []
+        for v in range(nv):
+            ns = C.c_int64()
+            check(LIB.korch_variant_cost(self.h, i, v, C.byref(ns)))
+            out.append(ns.value)
+        return out
+
     def set_variant(self, i: int, v: int):
         check(LIB.korch_select_variant(self.h, i, v))
 

@@ -211,17 +211,32 @@ KernelPlan generate_gemm(const Graph& g, const Candidate& c) {
   int64_t a_el = numel(va.shape), b_el = numel(vb.shape);
   kp.bytes = ep.bytes + 2 * (a_el + b_el);
 
-  // Tile widths: small BN spreads a skinny (small-M, weight-streaming) GEMM over more
-  // SMs; large BN maximises operand reuse.  The profiler keeps the fastest.
-  std::vector<int> bns;
+  // Launch configurations (the profiler keeps the fastest):
+  //  * tile width BN: small BN spreads a skinny (small-M, weight-streaming) GEMM over more
+  //    SMs, large BN maximises operand reuse;
+  //  * split-K (KS > 1) for grids far smaller than the 148 SMs: each CTA accumulates a
+  //    K-slice in TMEM, adds it into an fp32 scratch tile with red.global.add.v4.f32, and
+  //    the last CTA of the tile (arrival counter) runs the fused epilogue and re-zeroes
+  //    the scratch, so the kernel is self-cleaning across launches.
+  struct Cfg { int bn, ks; };
+  std::vector<Cfg> cfgs;
+  const int64_t NKt = (K + 63) / 64;
+  const int64_t Mt = (M + 127) / 128;
   if (has_reduce) {
-    // in-tile row reduction: one tile spans the whole row, each thread owns a row
-    bns.push_back((int)N);
+    cfgs.push_back({(int)N, 1});  // in-tile row reduction: one tile spans the whole row
   } else {
     for (int bn : {16, 32, 64, 128, 256})
-      if (bn <= 64 || bn / 2 < N) bns.push_back(bn);
+      if (bn <= 64 || bn / 2 < N) cfgs.push_back({bn, 1});
+    for (int bn : {32, 64, 128})
+      for (int ks : {2, 4, 8}) {
+        int64_t tiles = Mt * ((N + bn - 1) / bn) * batch;
+        if (bn > 64 && bn / 2 >= N) continue;
+        if (NKt % ks || tiles >= 148 || tiles * ks > 2 * 148 || N % 32 || N < bn) continue;
+        cfgs.push_back({bn, ks});
+      }
   }
-  for (int BN : bns) {
+  for (const Cfg& cf : cfgs) {
+    const int BN = cf.bn, KS = cf.ks;
     // epilogue chunk (TMEM columns per pass); the whole row when reducing
     const int CW = has_reduce ? BN : (BN < 32 ? BN : 32);
     GemmEpilogue epv;
@@ -244,12 +259,14 @@ KernelPlan generate_gemm(const Graph& g, const Candidate& c) {
     if (!b_kmaj) db.swizzle = b_swz_tma;
     const GemmEpilogue& ep = epv;
     const int A_BYTES = 128 * 64 * 2, B_BYTES = BN * 64 * 2, STAGE = A_BYTES + B_BYTES;
-    const int64_t NK = (K + 63) / 64;
+    const int64_t NK = NKt / KS;  // K-blocks per CTA
     // Pipeline depth: keep as many K-blocks in flight as shared memory allows (up to all
     // of them) -- small-M GEMMs are bound by TMA round-trip latency, not bandwidth.
     const int S = (int)std::max<int64_t>(2, std::min<int64_t>(NK, (200 * 1024) / STAGE));
     const int smem = S * STAGE + 1024 + (2 * S + 1) * 8 + 16;
     const int tcols = BN < 32 ? 32 : BN;
+    const int64_t Nt = (N + BN - 1) / BN;
+    const int64_t acc_bytes = ((batch * M * N * 4) + 255) / 256 * 256;
     uint32_t idesc = (1u << 4) | (1u << 7) | (1u << 10) | ((a_kmaj ? 0u : 1u) << 15) | ((b_kmaj ? 0u : 1u) << 16) |
                      ((uint32_t)(BN >> 3) << 17) | ((uint32_t)(128 >> 4) << 24);
     auto coords = [&](const std::string& inner, const std::string& outer, const std::vector<int>& baxes) {
@@ -262,8 +279,9 @@ KernelPlan generate_gemm(const Graph& g, const Candidate& c) {
     k << "extern \"C\" __global__ void __launch_bounds__(128, 1) KNAME(";
     for (size_t i = 0; i < kp.ext.size(); ++i)
       k << "const " << (g.dtype_of(kp.ext[i]) == DType::F32 ? "float" : "bf16_t") << "* __restrict__ p" << i << ", ";
-    k << (g.prims[c.output].dtype == DType::F32 ? "float" : "bf16_t") << "* __restrict__ out, "
-      << "const __grid_constant__ TmaMap tmA, const __grid_constant__ TmaMap tmB) {\n";
+    k << (g.prims[c.output].dtype == DType::F32 ? "float" : "bf16_t") << "* __restrict__ out, ";
+    if (KS > 1) k << "unsigned char* __restrict__ scratch, ";
+    k << "const __grid_constant__ TmaMap tmA, const __grid_constant__ TmaMap tmB) {\n";
     k << "  typedef int idx_t;\n";
     k << "  extern __shared__ __align__(1024) unsigned char smem_raw[];\n";
     k << "  unsigned char* smem = (unsigned char*)(((unsigned long long)smem_raw + 1023ull) & ~1023ull);\n";
@@ -273,7 +291,9 @@ KernelPlan generate_gemm(const Graph& g, const Candidate& c) {
     k << "  unsigned* tslot = (unsigned*)(accf + 1);\n";
     k << "  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;\n";
     k << "  const int tile_m = blockIdx.x * 128, tile_n = blockIdx.y * " << BN << ";\n";
-    k << "  int bzl = blockIdx.z;\n";
+    if (KS > 1) k << "  const int ks = blockIdx.z % " << KS << ";\n  int bzl = blockIdx.z / " << KS << ";\n";
+    else k << "  const int ks = 0;\n  int bzl = blockIdx.z;\n";
+    k << "  const int bzlin = bzl;\n  (void)bzlin; (void)ks;\n";
     for (int b = nbC - 1; b >= 0; --b) {
       k << "  const int " << ep.batch_vars[b] << " = bzl % " << C[b] << "; bzl /= " << C[b] << ";\n";
     }
@@ -288,7 +308,7 @@ KernelPlan generate_gemm(const Graph& g, const Candidate& c) {
     // producer
     k << "  if (warp == 0 && lane == 0) {\n";
     k << "    int s = 0; unsigned ph = 0;\n";
-    k << "    for (int kb = 0; kb < " << NK << "; ++kb) {\n";
+    k << "    for (int kb = ks * " << NK << "; kb < (ks + 1) * " << NK << "; ++kb) {\n";
     k << "      mbar_wait(empty + s, ph ^ 1u);\n";
     k << "      mbar_expect_tx(full + s, " << STAGE << "u);\n";
     k << "      unsigned char* sa = smem + s * " << STAGE << ";\n";
@@ -328,19 +348,58 @@ KernelPlan generate_gemm(const Graph& g, const Candidate& c) {
     k << "    tc_commit(accf);\n  }\n";
     // epilogue
     k << "  __syncwarp();\n  mbar_wait(accf, 0);\n  __syncwarp();\n  tc_fence_after();\n";
-    k << "  {\n    const int gm = tile_m + warp * 32 + lane;\n    const int tid = 0;\n    (void)tid;\n";
-    k << "    #pragma unroll 1\n    for (int ch = 0; ch < " << BN / CW << "; ++ch) {\n";
-    k << "      const int nb = tile_n + ch * " << CW << ";\n";
-    k << "      float acc[" << CW << "];\n";
-    if (CW <= 32) {
-      k << "      tc_ld" << CW << "(tmem + ((unsigned)(warp * 32) << 16) + (unsigned)(ch * " << CW << "), acc);\n";
+    k << "  const int gm = tile_m + warp * 32 + lane;\n";
+    auto tmem_load = [&]() {
+      std::ostringstream t;
+      if (CW <= 32) {
+        t << "      tc_ld" << CW << "(tmem + ((unsigned)(warp * 32) << 16) + (unsigned)(ch * " << CW << "), acc);\n";
+      } else {
+        t << "      #pragma unroll\n      for (int q = 0; q < " << CW / 32 << "; ++q)\n"
+          << "        tc_ld32(tmem + ((unsigned)(warp * 32) << 16) + (unsigned)(ch * " << CW << " + q * 32), acc + q * 32);\n";
+      }
+      return t.str();
+    };
+    if (KS == 1) {
+      k << "  {\n    const int tid = 0;\n    (void)tid;\n";
+      k << "    #pragma unroll 1\n    for (int ch = 0; ch < " << BN / CW << "; ++ch) {\n";
+      k << "      const int nb = tile_n + ch * " << CW << ";\n";
+      k << "      float acc[" << CW << "];\n";
+      k << tmem_load();
+      k << "      if (gm < " << M << " && nb < " << N << ") {\n";
+      k << ep.body << ep.store;
+      k << "      }\n    }\n  }\n";
     } else {
-      k << "      #pragma unroll\n      for (int q = 0; q < " << CW / 32 << "; ++q)\n"
-        << "        tc_ld32(tmem + ((unsigned)(warp * 32) << 16) + (unsigned)(ch * " << CW << " + q * 32), acc + q * 32);\n";
+      // 1) add this K-slice's partial tile into the fp32 scratch tile (L2 reductions)
+      k << "  float* wsa = reinterpret_cast<float*>(scratch) + (size_t)bzlin * " << M * N << ";\n";
+      k << "  unsigned* cnt = reinterpret_cast<unsigned*>(scratch + " << acc_bytes << ");\n";
+      k << "  const int tile_id = (bzlin * " << Nt << " + blockIdx.y) * " << Mt << " + blockIdx.x;\n";
+      k << "  #pragma unroll 1\n  for (int ch = 0; ch < " << BN / CW << "; ++ch) {\n";
+      k << "    float acc[" << CW << "];\n";
+      k << tmem_load();
+      k << "    if (gm < " << M << ") {\n      float* dst = wsa + (size_t)gm * " << N << " + tile_n + ch * " << CW << ";\n";
+      k << "      #pragma unroll\n      for (int q = 0; q < " << CW / 4 << "; ++q)\n";
+      k << "        asm volatile(\"red.global.add.v4.f32 [%0], {%1, %2, %3, %4};\" :: \"l\"(dst + 4 * q), "
+           "\"f\"(acc[4 * q]), \"f\"(acc[4 * q + 1]), \"f\"(acc[4 * q + 2]), \"f\"(acc[4 * q + 3]) : \"memory\");\n";
+      k << "    }\n  }\n";
+      // 2) the last CTA of this tile runs the epilogue on the full sum and re-zeroes it
+      k << "  __shared__ unsigned is_last;\n";
+      k << "  __threadfence();\n  __syncthreads();\n";
+      k << "  if (threadIdx.x == 0) is_last = atomicAdd(cnt + tile_id, 1u) == " << KS - 1 << "u;\n";
+      k << "  __syncthreads();\n";
+      k << "  if (is_last) {\n    __threadfence();\n    const int tid = 0;\n    (void)tid;\n";
+      k << "    #pragma unroll 1\n    for (int ch = 0; ch < " << BN / CW << "; ++ch) {\n";
+      k << "      const int nb = tile_n + ch * " << CW << ";\n";
+      k << "      float acc[" << CW << "];\n";
+      k << "      if (gm < " << M << ") {\n";
+      k << "        float* src = wsa + (size_t)gm * " << N << " + nb;\n";
+      k << "        #pragma unroll\n        for (int q = 0; q < " << CW / 4 << "; ++q) {\n";
+      k << "          const float4 t4 = __ldcg(reinterpret_cast<const float4*>(src + 4 * q));\n";
+      k << "          acc[4 * q] = t4.x; acc[4 * q + 1] = t4.y; acc[4 * q + 2] = t4.z; acc[4 * q + 3] = t4.w;\n";
+      k << "          __stcg(reinterpret_cast<float4*>(src + 4 * q), make_float4(0.f, 0.f, 0.f, 0.f));\n        }\n";
+      k << ep.body << ep.store;
+      k << "      }\n    }\n";
+      k << "    if (threadIdx.x == 0) cnt[tile_id] = 0u;\n  }\n";
     }
-    k << "      if (gm < " << M << " && nb < " << N << ") {\n";
-    k << ep.body << ep.store;
-    k << "      }\n    }\n  }\n";
     k << "  tc_fence_before();\n  __syncthreads();\n";
     k << "  if (warp == 2) tc_dealloc(tmem, " << tcols << ");\n}\n";
 
@@ -353,17 +412,17 @@ KernelPlan generate_gemm(const Graph& g, const Candidate& c) {
     src.replace(pos, 5, kv.name);
     kv.source = src;
     kv.block = 128;
-    kv.grid = 0;
-    kv.grid_y = (N + BN - 1) / BN;
-    kv.grid_z = batch;
-    kv.grid = (M + 127) / 128;
+    kv.grid = Mt;
+    kv.grid_y = Nt;
+    kv.grid_z = batch * KS;
     kv.smem = smem;
+    if (KS > 1) kv.scratch_bytes = acc_bytes + Mt * Nt * batch * 4;
     da.tensor = slotA;
     db.tensor = slotB;
     kv.tma = {da, db};
     std::ostringstream t;
-    t << "gemm BM=128 BN=" << BN << " BK=64 stages=" << S << " A=" << (a_kmaj ? "K" : "M") << "-major B="
-      << (b_kmaj ? "K" : "N") << "-major M=" << M << " N=" << N << " K=" << K << " batch=" << batch;
+    t << "gemm BM=128 BN=" << BN << " BK=64 splitK=" << KS << " stages=" << S << " A=" << (a_kmaj ? "K" : "M")
+      << "-major B=" << (b_kmaj ? "K" : "N") << "-major M=" << M << " N=" << N << " K=" << K << " batch=" << batch;
     kv.tag = t.str();
     kp.variants.push_back(kv);
   }

@@ -51,6 +51,7 @@ struct Module {
   bool compiled = false, failed = false;
   CUmodule mod = nullptr;
   CUfunction fn = nullptr;
+  CUdeviceptr scratch = 0;  // per-kernel scratch (split-K), zeroed once, kept zero by the kernel
   std::mutex mu;
 };
 
@@ -97,6 +98,7 @@ struct CandState {
   KernelPlan plan;
   int best = -1;          // chosen variant
   int64_t cost_ns = -1;
+  std::vector<int64_t> var_ns;  // per-variant profiled time (-1 = not profiled)
   std::string sig;
 };
 
@@ -259,6 +261,19 @@ static CUfunction load_fn(korch_ctx* ctx, Module* m, const KernelVariant& v) {
   return m->fn;
 }
 
+// Load the kernel and allocate its scratch; must run outside stream capture.
+static void prepare_variant(korch_ctx* ctx, const KernelVariant& v) {
+  Module* m = ctx->module_for(v.name);
+  load_fn(ctx, m, v);
+  std::lock_guard<std::mutex> lk(m->mu);
+  if (v.scratch_bytes > 0 && !m->scratch) {
+    CUresult r = cuda().cuMemAlloc(&m->scratch, (size_t)v.scratch_bytes);
+    if (r != CUDA_SUCCESS) throw KorchError(KORCH_E_OOM, "kernel scratch: " + cu_err(r));
+    CU_CHECK(cuda().cuMemsetD8Async(m->scratch, 0, (size_t)v.scratch_bytes, nullptr));
+    CU_CHECK(cuda().cuCtxSynchronize());
+  }
+}
+
 // ------------------------------------------------------------------ launching
 static void encode_tma(const TmaDesc& d, const void* base, CUtensorMap* out) {
   cuuint64_t dims[5], strides[4];
@@ -291,6 +306,11 @@ static void launch_variant(korch_ctx* ctx, const KernelPlan& plan, int vi, const
   }
   ptrs[ins.size()] = (CUdeviceptr)out;
   args.push_back(&ptrs[ins.size()]);
+  CUdeviceptr scratch = m->scratch;
+  if (v.scratch_bytes > 0) {
+    if (!scratch) throw KorchError(KORCH_E_CUDA, "kernel scratch not prepared: " + v.name);
+    args.push_back(&scratch);
+  }
   std::vector<CUtensorMap> maps(v.tma.size());
   for (size_t t = 0; t < v.tma.size(); ++t) {
     const TmaDesc& d = v.tma[t];
@@ -363,8 +383,10 @@ korch_status korch_destroy(korch_ctx* c) {
   if (c->gpu && cuda().ok) {
     cuda().cuCtxSetCurrent(c->cuctx);
     cuda().cuCtxSynchronize();
-    for (auto& kv : c->modules)
+    for (auto& kv : c->modules) {
       if (kv.second->mod) cuda().cuModuleUnload(kv.second->mod);
+      if (kv.second->scratch) cuda().cuMemFree(kv.second->scratch);
+    }
     if (c->arena) cuda().cuMemFree(c->arena);
     if (c->flush) cuda().cuMemFree(c->flush);
     if (c->pstream) cuda().cuStreamDestroy(c->pstream);
@@ -554,11 +576,13 @@ korch_status korch_profile(korch_graph* G, const int64_t* idx, int64_t n, const 
       int64_t best = INT64_MAX;
       int bestv = -1;
       int nv = tune ? (int)s.plan.variants.size() : 1;
+      s.var_ns.assign(s.plan.variants.size(), -1);
       for (int vi = 0; vi < nv; ++vi) {
         Module* m = ctx->module_for(s.plan.variants[vi].name);
         if (!m->compiled) continue;
         try {
           int nl = flush ? 1 : launches;
+          prepare_variant(ctx, s.plan.variants[vi]);
           CU_CHECK(cu.cuStreamBeginCapture(ctx->pstream, CU_STREAM_CAPTURE_MODE_THREAD_LOCAL));
           try {
             for (int l = 0; l < nl; ++l) launch_variant(ctx, s.plan, vi, ins, outp, ctx->pstream);
@@ -589,6 +613,7 @@ korch_status korch_profile(korch_graph* G, const int64_t* idx, int64_t n, const 
           std::sort(ts.begin(), ts.end());
           int64_t ns = (int64_t)std::llround((double)ts[ts.size() / 2] * 1e6);
           if (ns < 1) ns = 1;
+          s.var_ns[vi] = ns;
           if (ns < best) { best = ns; bestv = vi; }
         } catch (KorchError& e) {
           // a variant that fails to launch is rejected (cost = inf for it)
@@ -620,6 +645,15 @@ korch_status korch_variant_info(const korch_graph* G, int64_t i, int32_t* nv, in
     size_t need;
     return write_buf(t, tag, cap, &need);
   }
+  return KORCH_OK;
+}
+
+korch_status korch_variant_cost(const korch_graph* G, int64_t i, int32_t v, int64_t* ns) {
+  if (!G || !ns) return fail(KORCH_E_ARG, "NULL argument");
+  if (i < 0 || i >= (int64_t)G->cands.size()) return fail(KORCH_E_ARG, "candidate index out of range");
+  const CandState& s = G->cs[i];
+  if (v < 0 || v >= (int32_t)s.plan.variants.size()) return fail(KORCH_E_ARG, "variant index out of range");
+  *ns = v < (int32_t)s.var_ns.size() ? s.var_ns[v] : -1;
   return KORCH_OK;
 }
 
@@ -776,6 +810,8 @@ korch_status korch_execute(korch_graph* G, const void* const* inputs, void* cons
     };
     static const bool direct = getenv("KORCH_EXEC_DIRECT") != nullptr;
     static const bool use_pdl = !(getenv("KORCH_PDL") && std::string(getenv("KORCH_PDL")) == "0");
+    if (direct || !G->gexec || ptrs != G->cap_ptrs)
+      for (auto& st : G->steps) prepare_variant(ctx, G->cs[st.cand].plan.variants[st.variant]);
     if (direct) {  // plain stream launches (profilers that cannot follow graph replays)
       for (auto& st : G->steps) {
         std::vector<const void*> ins;
