@@ -63,6 +63,8 @@ typedef struct {
   int32_t max_prims;          /* reject candidates with more primitives; default 16 */
   int32_t keep_multi_linear;  /* 1 = keep candidates with >= 2 dense linear prims; default 0 */
   int64_t max_states;         /* KORCH_E_STATE_EXPLOSION above this; default 1,000,000       */
+  int32_t partition_max;      /* > 0: partition (reading A17) into parts of about this
+                                 many primitives; 0: only graphs > 256 primitives, parts of 64 */
 } korch_enum_opts;
 
 /* One candidate kernel (P', o): a convex set with a unique sink o (reading A4). */
@@ -79,6 +81,7 @@ typedef struct {
   int64_t bytes;              /* algorithmic HBM bytes: external inputs read + output       */
   double flops;               /* 2*M*N*K summed over dense linear members                   */
   const char* signature;      /* canonical text of the generated kernel (dedup key)         */
+  int32_t part;               /* partition part the candidate lies in (0 if unpartitioned)  */
 } korch_cand_desc;
 
 /* Options for korch_profile (reading A19). Zero-initialised fields take the defaults. */

@@ -154,6 +154,78 @@ def candidates(g: PGraph, convex_sets, max_prims=16, prune_linear=True):
     return out
 
 
+def partition(g: PGraph, max_nodes: int = 64):
+    """Reading A17 (P:121 leaves the rule unspecified): cut only at articulation tensors.
+
+    A cut may follow position i of the topological order (Kahn, smallest id first) when
+    exactly one primitive of the prefix topo[0..i] is consumed after it.  Parts are grown
+    greedily: when a part would exceed max_nodes it is closed at the latest cut inside
+    it; a part without any cut grows past max_nodes.  Returns lists of primitive ids."""
+    topo = g.topo
+    n = len(topo)
+    pos = {v: i for i, v in enumerate(topo)}
+    last_use = [max((pos[w] for w in g.succs[v]), default=-1) for v in topo]
+    cut_after = []
+    active = 0
+    ends = [0] * (n + 1)
+    for i, v in enumerate(topo):
+        if last_use[i] > i:
+            active += 1
+            ends[last_use[i]] += 1
+        active -= ends[i]
+        cut_after.append(active == 1 and i < n - 1)
+    parts, start, last_cut = [], 0, None
+    for i in range(n):
+        if i - start + 1 > max_nodes and last_cut is not None and last_cut >= start:
+            parts.append(topo[start:last_cut + 1])
+            start = last_cut + 1
+            last_cut = None
+            for j in range(start, i):       # cuts between the new start and i
+                if cut_after[j]:
+                    last_cut = j
+        if cut_after[i]:
+            last_cut = i
+    parts.append(topo[start:])
+    return [sorted(p) for p in parts]
+
+
+def candidates_partitioned(g: PGraph, parts, max_prims=16, prune_linear=True):
+    """Candidates of every part (convex unique-sink sets inside one part), canonical order.
+
+    A set inside one part is convex in G iff it is convex in the part: a path leaving a
+    part through its cut tensor never returns to it."""
+    out = []
+    n_states = 0
+    for part in parts:
+        ps = set(part)
+        idx = {v: i for i, v in enumerate(part)}
+        ext_specs = {}
+        sub_nodes = []
+        for v in part:
+            nd = dict(g.pg["nodes"][v])
+            ins = []
+            for r in nd["inputs"]:
+                if r[0] == "node" and r[1] not in ps:   # produced by an earlier part
+                    name = f"__p{r[1]}"
+                    ext_specs[name] = {"name": name, "shape": list(g.pg["nodes"][r[1]]["shape"])}
+                    ins.append(("input", name))
+                elif r[0] == "node":
+                    ins.append(("node", idx[r[1]]))
+                else:
+                    ins.append(r)
+            sub_nodes.append(dict(nd, id=idx[v], inputs=ins))
+        local = {"nodes": sub_nodes, "outputs": [],
+                 "inputs": list(g.pg.get("inputs", [])) + list(ext_specs.values())}
+        sg = PGraph(local)
+        st = execution_states(sg)
+        n_states += len(st)
+        back = {i: v for v, i in idx.items()}
+        for members, o in candidates(sg, convex_sets_from_states(st), max_prims, prune_linear):
+            out.append((tuple(sorted(back[m] for m in members)), back[o]))
+    out.sort(key=lambda c: (c[1], len(c[0]), c[0]))
+    return out, n_states
+
+
 def candidate_inputs(g: PGraph, members):
     """Primitive inputs of a candidate: nodes outside P' feeding P' (the I matrix row)."""
     m = set(members)

@@ -19,7 +19,7 @@ import os
 
 from . import _lib
 from ._lib import LIB, check
-from .select import INF, operator_aligned, singletons, solve_blp
+from .select import INF, operator_aligned, singletons, solve_blp, solve_partitioned
 
 DTYPE_BYTES = {"f32": 4, "bf16": 2}
 
@@ -84,8 +84,9 @@ class KorchGraph:
         return tuple(self.prim["nodes"][self.outputs[k]]["shape"])
 
     # ---------------------------------------------------------------- candidates
-    def enumerate(self, max_prims: int = 16, keep_multi_linear: bool = False, max_states: int = 1_000_000):
-        o = _lib.EnumOpts(max_prims, int(keep_multi_linear), max_states)
+    def enumerate(self, max_prims: int = 16, keep_multi_linear: bool = False, max_states: int = 1_000_000,
+                  partition_max: int = 0):
+        o = _lib.EnumOpts(max_prims, int(keep_multi_linear), max_states, partition_max)
         nc, ns = C.c_int64(), C.c_int64()
         check(LIB.korch_enumerate(self.h, C.byref(o), C.byref(nc), C.byref(ns)))
         self.n_states = ns.value
@@ -106,6 +107,7 @@ class KorchGraph:
             "bytes": d.bytes,
             "flops": d.flops,
             "signature": d.signature.decode(),
+            "part": d.part,
         }
 
     def source(self, i: int) -> str:
@@ -142,8 +144,9 @@ class KorchGraph:
 
     # ---------------------------------------------------------------- orchestration
     def select(self, costs=None, time_limit=600.0):
+        """Eq. 2-4 optimum (per partition part when the graph was partitioned)."""
         costs = self.costs if costs is None else costs
-        return solve_blp(self.cands, costs, self.outputs, time_limit=time_limit)
+        return solve_partitioned(self.cands, costs, self.outputs, time_limit=time_limit)
 
     def operator_aligned(self):
         return operator_aligned(self.cands, self.prim)

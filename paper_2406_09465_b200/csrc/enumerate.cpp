@@ -2,6 +2,11 @@
 // two states (Theorem 1) with a unique sink (readings A3/A4), pruned as
 // in P:626 ("too many operators ... or including multiple linear transformation
 // primitives", reading A5/A18) and put in canonical order.
+//
+// Whole models are first partitioned (reading A17): cuts only at articulation
+// tensors of the topological order, parts grown greedily to `partition_max` primitives,
+// and Alg. 1 runs inside each part (a set inside one part is convex in G iff it is
+// convex in the part, since a path that leaves a part never returns).
 #include "enumerate.h"
 
 #include <algorithm>
@@ -13,17 +18,12 @@ namespace korch {
 
 namespace {
 struct Dfs {
-  const Graph& g;
+  int n;
   int64_t cap;
-  std::vector<Bits> pred_bits;
+  std::vector<Bits> pred_bits;           // local indices
   std::unordered_set<Bits, BitsHash> B;  // database of execution states
   std::vector<Bits> order;               // insertion order (deterministic)
-  Dfs(const Graph& gg, int64_t c) : g(gg), cap(c) {
-    int n = (int)g.prims.size();
-    pred_bits.resize(n);
-    for (int v = 0; v < n; ++v)
-      for (int u : g.preds[v]) pred_bits[v].set(u);
-  }
+  Dfs(int nn, int64_t c) : n(nn), cap(c), pred_bits(nn) {}
   bool ready(const Bits& X, int v) const {  // forall (u,v) in E: u in X
     for (int i = 0; i < kMaxPrims / 64; ++i)
       if (pred_bits[v].w[i] & ~X.w[i]) return false;
@@ -34,7 +34,6 @@ struct Dfs {
     while (!stack.empty()) {
       Bits cur = stack.back();
       stack.pop_back();
-      int n = (int)g.prims.size();
       for (int v = n - 1; v >= 0; --v) {
         if (cur.test(v) || !ready(cur, v)) continue;
         Bits nx = cur;
@@ -52,66 +51,122 @@ struct Dfs {
 };
 }  // namespace
 
-std::vector<Candidate> enumerate_candidates(const Graph& g, const EnumOpts& o, int64_t* n_states) {
+std::vector<std::vector<int>> partition_graph(const Graph& g, int max_nodes) {
   int n = (int)g.prims.size();
-  if (n > kMaxPrims)
-    throw KorchError(KORCH_E_ARG, "primitive graph has " + std::to_string(n) +
-                                      " nodes; partition it to <= 256 first");
-  Dfs d(g, o.max_states);
-  Bits empty;
-  d.B.insert(empty);  // reading A1: seed B with the empty state
-  d.order.push_back(empty);
-  d.run(empty);
-  if (n_states) *n_states = (int64_t)d.order.size();
+  const std::vector<int>& topo = g.topo;
+  std::vector<int> last_use(n, -1), ends(n + 1, 0);
+  for (int i = 0; i < n; ++i)
+    for (int w : g.succs[topo[i]]) last_use[i] = std::max(last_use[i], g.topo_index[w]);
+  std::vector<char> cut_after(n, 0);
+  int active = 0;
+  for (int i = 0; i < n; ++i) {
+    if (last_use[i] > i) {
+      ++active;
+      ++ends[last_use[i]];
+    }
+    active -= ends[i];
+    cut_after[i] = active == 1 && i < n - 1;
+  }
+  std::vector<std::vector<int>> parts;
+  int start = 0, last_cut = -1;
+  for (int i = 0; i < n; ++i) {
+    if (i - start + 1 > max_nodes && last_cut >= start) {
+      parts.emplace_back(topo.begin() + start, topo.begin() + last_cut + 1);
+      start = last_cut + 1;
+      last_cut = -1;
+      for (int j = start; j < i; ++j)
+        if (cut_after[j]) last_cut = j;
+    }
+    if (cut_after[i]) last_cut = i;
+  }
+  parts.emplace_back(topo.begin() + start, topo.end());
+  for (auto& p : parts) std::sort(p.begin(), p.end());
+  return parts;
+}
 
-  std::vector<Bits> succ_bits(n);
-  for (int v = 0; v < n; ++v)
-    for (int w : g.succs[v]) succ_bits[v].set(w);
+std::vector<Candidate> enumerate_candidates(const Graph& g, const EnumOpts& o, int64_t* n_states,
+                                            std::vector<std::vector<int>>* parts_out) {
+  int n = (int)g.prims.size();
+  int pmax = o.partition_max > 0 ? o.partition_max : (n > kMaxPrims ? 64 : 0);
+  std::vector<std::vector<int>> parts;
+  if (pmax > 0) {
+    parts = partition_graph(g, pmax);
+  } else {
+    parts.emplace_back();
+    for (int v = 0; v < n; ++v) parts.back().push_back(v);
+  }
+  for (auto& p : parts)
+    if ((int)p.size() > kMaxPrims)
+      throw KorchError(KORCH_E_ARG, "a partition part has " + std::to_string(p.size()) +
+                                        " primitives (> 256); no articulation tensor to cut at");
   std::vector<char> dense(n);
   for (int v = 0; v < n; ++v) dense[v] = g.is_dense_linear(v);
-
-  // for D1 subset D2: P' = D2 \ D1; keep unique-sink sets once.
-  std::unordered_set<Bits, BitsHash> seen;
   std::vector<Candidate> out;
-  const auto& S = d.order;
-  for (size_t a = 0; a < S.size(); ++a) {
-    for (size_t b = 0; b < S.size(); ++b) {
-      if (!S[a].subset_of(S[b])) continue;
-      Bits P = S[b].minus(S[a]);
-      int cnt = P.count();
-      if (cnt > o.max_prims) continue;
-      if (!seen.insert(P).second) continue;
-      int sink = -1, nsink = 0, nd = 0;
-      for (int v : P.list()) {
-        bool internal_succ = false;
-        for (int i = 0; i < kMaxPrims / 64; ++i)
-          if (succ_bits[v].w[i] & P.w[i]) { internal_succ = true; break; }
-        if (!internal_succ) { sink = v; ++nsink; }
-        nd += dense[v];
-      }
-      if (nsink != 1) continue;                         // single output (A4)
-      if (!o.keep_multi_linear && nd >= 2) continue;    // P:626 (A18)
-      Candidate c;
-      c.members = P.list();
-      c.output = sink;
-      c.n_dense = nd;
-      std::vector<int> ins;
-      std::vector<int> gins;
-      for (int v : c.members) {
-        for (auto& r : g.prims[v].in) {
-          if (r.is_input) gins.push_back(r.id);
-          else if (!P.test(r.id)) ins.push_back(r.id);
+  int64_t total_states = 0;
+  for (size_t pi = 0; pi < parts.size(); ++pi) {
+    const std::vector<int>& part = parts[pi];
+    int m = (int)part.size();
+    std::vector<int> loc(n, -1);
+    for (int i = 0; i < m; ++i) loc[part[i]] = i;
+    Dfs d(m, o.max_states);
+    std::vector<Bits> succ_bits(m);
+    for (int i = 0; i < m; ++i) {
+      for (int u : g.preds[part[i]])
+        if (loc[u] >= 0) d.pred_bits[i].set(loc[u]);
+      for (int w : g.succs[part[i]])
+        if (loc[w] >= 0) succ_bits[i].set(loc[w]);
+    }
+    Bits empty;
+    d.B.insert(empty);  // reading A1: seed B with the empty state
+    d.order.push_back(empty);
+    d.run(empty);
+    total_states += (int64_t)d.order.size();
+    // for D1 subset D2: P' = D2 \ D1; keep unique-sink sets once.
+    std::unordered_set<Bits, BitsHash> seen;
+    const auto& S = d.order;
+    for (size_t a = 0; a < S.size(); ++a) {
+      for (size_t b = 0; b < S.size(); ++b) {
+        if (!S[a].subset_of(S[b])) continue;
+        Bits P = S[b].minus(S[a]);
+        if (P.count() > o.max_prims) continue;
+        if (!seen.insert(P).second) continue;
+        int sink = -1, nsink = 0, nd = 0;
+        std::vector<int> mem_local = P.list();
+        for (int v : mem_local) {
+          bool internal_succ = false;
+          for (int i = 0; i < kMaxPrims / 64; ++i)
+            if (succ_bits[v].w[i] & P.w[i]) { internal_succ = true; break; }
+          if (!internal_succ) { sink = v; ++nsink; }
+          nd += dense[part[v]];
         }
+        if (nsink != 1) continue;                         // single output (A4)
+        if (!o.keep_multi_linear && nd >= 2) continue;    // P:626 (A18)
+        Candidate c;
+        for (int v : mem_local) c.members.push_back(part[v]);
+        std::sort(c.members.begin(), c.members.end());
+        c.output = part[sink];
+        c.n_dense = nd;
+        c.part = (int)pi;
+        std::vector<int> ins, gins;
+        std::vector<char> in_p(n, 0);
+        for (int v : c.members) in_p[v] = 1;
+        for (int v : c.members)
+          for (auto& r : g.prims[v].in) {
+            if (r.is_input) gins.push_back(r.id);
+            else if (!in_p[r.id]) ins.push_back(r.id);
+          }
+        std::sort(ins.begin(), ins.end());
+        ins.erase(std::unique(ins.begin(), ins.end()), ins.end());
+        std::sort(gins.begin(), gins.end());
+        gins.erase(std::unique(gins.begin(), gins.end()), gins.end());
+        c.inputs = ins;
+        c.graph_inputs = gins;
+        out.push_back(std::move(c));
       }
-      std::sort(ins.begin(), ins.end());
-      ins.erase(std::unique(ins.begin(), ins.end()), ins.end());
-      std::sort(gins.begin(), gins.end());
-      gins.erase(std::unique(gins.begin(), gins.end()), gins.end());
-      c.inputs = ins;
-      c.graph_inputs = gins;
-      out.push_back(std::move(c));
     }
   }
+  if (n_states) *n_states = total_states;
+  if (parts_out) *parts_out = parts;
   std::sort(out.begin(), out.end(), [](const Candidate& x, const Candidate& y) {
     if (x.output != y.output) return x.output < y.output;
     if (x.members.size() != y.members.size()) return x.members.size() < y.members.size();

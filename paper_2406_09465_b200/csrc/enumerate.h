@@ -63,16 +63,22 @@ struct Candidate {
   double flops = 0;
   std::string signature;
   std::string reject_reason;
+  int part = 0;                   // partition part (A17)
 };
 
 struct EnumOpts {
   int max_prims = 16;
   bool keep_multi_linear = false;
   int64_t max_states = 1000000;
+  int partition_max = 0;          // > 0: partition into parts of about this many primitives
 };
 
-// Runs Alg. 1 with B seeded with the empty state (reading A1); returns the
-// unique-sink, pruned candidates in canonical order and the state count.
-std::vector<Candidate> enumerate_candidates(const Graph& g, const EnumOpts& o, int64_t* n_states);
+// Reading A17: parts of the topological order separated at articulation tensors.
+std::vector<std::vector<int>> partition_graph(const Graph& g, int max_nodes);
+
+// Runs Alg. 1 (per partition part) with B seeded with the empty state (reading A1);
+// returns the unique-sink, pruned candidates in canonical order and the state count.
+std::vector<Candidate> enumerate_candidates(const Graph& g, const EnumOpts& o, int64_t* n_states,
+                                            std::vector<std::vector<int>>* parts = nullptr);
 
 }  // namespace korch

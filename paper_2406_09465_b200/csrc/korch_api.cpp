@@ -450,6 +450,7 @@ korch_status korch_enumerate(korch_graph* G, const korch_enum_opts* o, int64_t* 
       if (o->max_prims > 0) eo.max_prims = o->max_prims;
       eo.keep_multi_linear = o->keep_multi_linear != 0;
       if (o->max_states > 0) eo.max_states = o->max_states;
+      if (o->partition_max > 0) eo.partition_max = o->partition_max;
     }
     std::lock_guard<std::mutex> lk(G->mu);
     G->cands = enumerate_candidates(G->g, eo, &G->n_states);
@@ -479,6 +480,7 @@ korch_status korch_candidate(const korch_graph* G, int64_t i, korch_cand_desc* d
   d->bytes = c.bytes;
   d->flops = c.flops;
   d->signature = c.signature.c_str();
+  d->part = c.part;
   return KORCH_OK;
 }
 

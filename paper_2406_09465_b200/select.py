@@ -60,6 +60,38 @@ def solve_blp(cands, costs, outputs, time_limit=600.0):
     return int(sum(costs[i] for i in sel)), sel
 
 
+def solve_partitioned(cands, costs, outputs, time_limit=600.0):
+    """Per-part decomposition of the BLP (parts from partitioning, reading A17).
+
+    Parts interact only through cut tensors (a part's primitives consumed by a later
+    part), so the global optimum is the sum of per-part optima with
+    T_part = (graph outputs in the part) + (its primitives consumed by later parts)."""
+    parts = sorted({c.get("part", 0) for c in cands})
+    if len(parts) <= 1:
+        return solve_blp(cands, costs, outputs, time_limit)
+    part_of = {}
+    for c in cands:
+        for m in c["members"]:
+            part_of[m] = c.get("part", 0)
+    needed_by_later = set()
+    for c in cands:
+        for j in c["inputs"]:
+            if part_of.get(j, c["part"]) != c["part"]:
+                needed_by_later.add(j)
+    total, sel = 0, []
+    for p in parts:
+        idx = [i for i, c in enumerate(cands) if c.get("part", 0) == p]
+        sub = [cands[i] for i in idx]
+        members = {m for c in sub for m in c["members"]}
+        t_p = sorted(({o for o in outputs if o in members} | needed_by_later) & members)
+        # inputs produced by earlier parts are available (their T made them so)
+        sub_local = [dict(c, inputs=[j for j in c["inputs"] if j in members]) for c in sub]
+        obj, s = solve_blp(sub_local, [costs[i] for i in idx], t_p, time_limit)
+        total += obj
+        sel.extend(idx[k] for k in s)
+    return total, sorted(sel)
+
+
 def operator_aligned(cands, prim_graph):
     """The 'one kernel per unfused operator' orchestration: for every
     operator, the candidate whose members are exactly that operator's fission fragment."""

@@ -162,6 +162,40 @@ def test_blp_matches_exact_search_c1(ctx):
         kg.set_orchestration(sel)          # the library accepts it (Eq. 3/4)
 
 
+@pytest.mark.parametrize("name,pm", [("c2", 8), ("c2", 12), ("c2_r1r3", 10), ("misc", 6), ("c1", 5)])
+def test_partitioned_enumeration_matches_oracle(ctx, name, pm):
+    from oracle.enumeration import candidates_partitioned, partition
+    g = GRAPHS[name]()
+    kg = KorchGraph(ctx, g)
+    ours = kg.enumerate(partition_max=pm)
+    G = PGraph(fission(g))
+    parts = partition(G, pm)
+    ref, n_states = candidates_partitioned(G, parts)
+    assert [(tuple(c["members"]), c["output"]) for c in ours] == [(tuple(m), o) for m, o in ref]
+    assert kg.n_states == n_states
+    part_of = {v: i for i, p in enumerate(parts) for v in p}
+    assert all(part_of[c["output"]] == c["part"] for c in ours)
+
+
+def test_partitioned_blp_equals_global_optimum(ctx):
+    """Per-part decomposition of Eq. 2-4 reaches the optimum of the whole (partitioned)
+    candidate set (oracle producer-assignment search over all parts at once)."""
+    g = c1_softmax_layernorm()
+    kg = KorchGraph(ctx, g)
+    ours = kg.enumerate(partition_max=5)
+    assert len({c["part"] for c in ours}) > 1
+    G = PGraph(fission(g))
+    ref = [(tuple(c["members"]), c["output"]) for c in ours]
+    cin = [candidate_inputs(G, m) for m, _ in ref]
+    rng = np.random.default_rng(21)
+    for _ in range(3):
+        costs = [int(1500 + 90 * len(c["members"]) + rng.integers(0, 700)) for c in ours]
+        obj, sel = kg.select(costs)
+        best, _ = producer_search(ref, costs, G.pg["outputs"], cin, G.topo_index)
+        assert obj == best
+        assert feasible(ref, sel, G.pg["outputs"], cin)
+
+
 def test_blp_with_rejections_and_baselines(ctx):
     g = c2_vit_attention()
     kg = KorchGraph(ctx, g)

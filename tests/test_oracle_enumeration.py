@@ -96,6 +96,38 @@ def test_config_golden_counts():
             assert len(candidates(g, cs, 12)) == case["pruned12"]
 
 
+def test_partition_pins():
+    """Reading A17: cuts only at articulation tensors; SPEC S:102 chain example."""
+    from oracle.enumeration import partition
+    chain = PGraph.from_edges(6, [(i, i + 1) for i in range(5)])
+    assert partition(chain, 3) == [[0, 1, 2], [3, 4, 5]]                  # S:102
+    diamond = PGraph.from_edges(4, [(0, 1), (0, 2), (1, 3), (2, 3)])
+    assert partition(diamond, 2) == [[0], [1, 2, 3]]                       # only `a` is a cut tensor
+    two = PGraph.from_edges(8, [(0, 1), (0, 2), (1, 3), (2, 3), (3, 4), (4, 5), (4, 6), (5, 7), (6, 7)])
+    parts = partition(two, 4)
+    assert sorted(v for p in parts for v in p) == list(range(8))
+    for p in parts[:-1]:                                                   # one tensor crosses each cut
+        later = {v for q in parts[parts.index(p) + 1:] for v in q}
+        crossing = {u for u in p if any(w in later for w in two.succs[u])}
+        assert len(crossing) == 1
+    assert partition(two, 100) == [list(range(8))]
+
+
+def test_partitioned_candidates_are_global_candidates():
+    """Every within-part candidate is a convex unique-sink set of the whole graph."""
+    from oracle.enumeration import candidates_partitioned, partition
+    pg = fission(c2_vit_attention(seq=16, hidden=64, heads=4))
+    g = PGraph(pg)
+    glob = set(candidates(g, convex_sets_from_states(execution_states(g))))
+    for pm in (6, 10, 16):
+        parts = partition(g, pm)
+        cands, _ = candidates_partitioned(g, parts)
+        assert set(cands) <= glob
+        for members, o in cands:
+            assert is_convex(g, set(members))
+            assert len({next(i for i, p in enumerate(parts) if m in p) for m in members}) == 1
+
+
 def test_unique_sink_members_reach_output():
     """Reading A4: every member of a unique-sink candidate reaches its output."""
     pg = fission(c2_vit_attention(seq=16, hidden=64, heads=4))
