@@ -141,6 +141,87 @@ def oracle_baseline(graph, sel_cands, sel, budget_s=15.0):
             "sample": f"{n} inferences of the selected orchestration (fp64 numpy, bf16/fp32 rounding at kernel outputs), {el:.1f} s"}
 
 
+def time_plan(kg, sel, dev_in, steps=20, flush_mb=512):
+    """Mean device ms per execution of orchestration `sel` (CUDA events on the launch
+    stream, L2 flushed between steps outside the events)."""
+    import torch
+    kg.set_orchestration(sel)
+    outs, ws = kg.torch_outputs(), kg.torch_workspace()
+    stream = torch.cuda.current_stream()
+    flush = torch.empty(flush_mb << 20, dtype=torch.uint8, device="cuda")
+    for _ in range(3):
+        kg.execute(dev_in, outs, ws, stream)
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(steps)]
+    torch.cuda.synchronize()
+    for i, (a, e) in enumerate(ev):
+        flush.fill_(i & 0xFF)
+        a.record(stream)
+        kg.execute(dev_in, outs, ws, stream)
+        e.record(stream)
+    torch.cuda.synchronize()
+    return statistics.mean(a.elapsed_time(e) for a, e in ev), outs
+
+
+def run_models(K, names, oracle_check=True):
+    """Whole paper models at their paper input sizes, bs = 1: partition,
+    enumerate, compile, profile, BLP-select, then measure the chosen orchestration and the
+    operator-aligned one (one kernel per unfused operator) end to end."""
+    import numpy as np
+    import torch
+    from korch_workloads import make_inputs
+    from korch_workloads.models import MODELS
+    os.environ["KORCH_CACHE_DIR"] = os.environ.get("KORCH_MODEL_CACHE", "/tmp/korch_model_cache")
+    os.makedirs(os.environ["KORCH_CACHE_DIR"], exist_ok=True)
+    res = {}
+    for name in names:
+        t0 = time.perf_counter()
+        graph = MODELS[name]()
+        ctx = K.Context(torch.cuda.current_device())
+        kg = K.KorchGraph(ctx, graph)
+        cands = kg.enumerate(partition_max=64)
+        t_enum = time.perf_counter() - t0
+        t1 = time.perf_counter()
+        kg.compile()
+        t_comp = time.perf_counter() - t1
+        t1 = time.perf_counter()
+        costs = kg.profile()
+        t_prof = time.perf_counter() - t1
+        t1 = time.perf_counter()
+        obj, sel = kg.select(costs)
+        t_sel = time.perf_counter() - t1
+        base = kg.operator_aligned()
+        ins = make_inputs(graph, seed=0)
+        dev = K.torch_inputs(graph, {k: v[1] for k, v in ins.items()})
+        ms_sel, outs = time_plan(kg, sel, dev)
+        got = [o.float().cpu().numpy().astype(np.float64) for o in outs]
+        ms_base, _ = time_plan(kg, base, dev)
+        entry = {"input": graph["inputs"][0]["shape"], "n_prims": kg.n_prims, "n_candidates": len(cands),
+                 "n_generable": len(kg.generable()), "n_states": kg.n_states,
+                 "parts": len({c["part"] for c in cands}),
+                 "latency_ms": ms_sel, "kernels": len(sel),
+                 "operator_aligned_ms": ms_base, "operator_aligned_kernels": len(base),
+                 "speedup_vs_operator_aligned": ms_base / ms_sel,
+                 "blp_objective_ns": obj, "operator_aligned_objective_ns": sum(costs[i] for i in base),
+                 "tuning_s": {"enumerate": t_enum, "compile": t_comp, "profile": t_prof, "select": t_sel}}
+        if oracle_check:
+            from oracle.enumeration import PGraph
+            from oracle.evaluate import eval_orchestration
+            from oracle.fission import fission
+            t1 = time.perf_counter()
+            pg = fission(graph)
+            G = PGraph(pg)
+            want = eval_orchestration(pg, [(tuple(c["members"]), c["output"]) for c in cands], sel,
+                                      {k: v[0] for k, v in ins.items()}, G.topo_index, graph["dtype"])
+            errs = [float(np.max(np.abs(g - want[o])) / np.max(np.abs(want[o]))) for g, o in zip(got, kg.outputs)]
+            entry["oracle_rel_err"] = max(errs)
+            entry["oracle_s"] = time.perf_counter() - t1
+        res[name] = entry
+        del kg, outs, dev
+        ctx.close()
+        torch.cuda.empty_cache()
+    return res
+
+
 def bandwidth_variant(K, pk, steps=10):
     """C1 at x[2^20,128] fp32 (SURVEY.md §8(d) C1 bandwidth variant): enumerate, profile
     (cold, inputs > L2), BLP-select, execute; achieved GB/s of the plan and of its
@@ -225,6 +306,7 @@ def main():
     ap.add_argument("--impl", default="korch", choices=["korch", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-bw-variant", action="store_true", help="skip the C1 x[2^20,128] bandwidth measurement")
+    ap.add_argument("--models", default="", help="comma list of whole models to tune and time (candy,segformer)")
     ap.add_argument("--cpu-budget", type=float, default=15.0)
     ap.add_argument("--save-selection", default=None, help="write the chosen plan (for tools/replay.py)")
     args = ap.parse_args()
@@ -386,6 +468,14 @@ def main():
     from paper_2406_09465_b200.dist import max_over_ranks
     ms_max, e2e_max = max_over_ranks([ms, e2e_ms], device="cuda")
 
+    # the operator-aligned orchestration measured end to end (BASELINE target)
+    base_ms = None
+    if base_obj is not None:
+        base_ms, _ = time_plan(kg, base, dev_in, steps=args.steps)
+        kg.set_orchestration(sel)
+    models = None
+    if rank == 0 and world == 1 and args.models:
+        models = run_models(K, [m for m in args.models.split(",") if m])
     bw = None
     if rank == 0 and world == 1 and not args.no_bw_variant:
         try:
@@ -408,7 +498,10 @@ def main():
             "gpu_launches": len(order) * args.steps,
             "kernels_per_step": len(order),
             "selection": {"blp_objective_ns": obj, "operator_aligned_ns": base_obj,
-                          "operator_aligned_kernels": len(base), "kernels": order},
+                          "operator_aligned_kernels": len(base), "kernels": order,
+                          "operator_aligned_ms": base_ms,
+                          "speedup_vs_operator_aligned": (base_ms / ms_max) if base_ms else None},
+            "models": models,
             "roofline": roof,
             "bandwidth_variant": bw,
             "cpu_baseline": cpu,

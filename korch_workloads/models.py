@@ -1,0 +1,167 @@
+"""Operator graphs of the paper's whole-model workloads, synthetic weights.
+
+Architectures follow SURVEY.md §8(d) (public model definitions, treated as proposals):
+  candy       fast-neural-style TransformerNet (artifact model P:741-743) at 224^2:
+              reflect-pad + conv, InstanceNorm(affine), ReLU, 5 residual blocks,
+              nearest x2 upsample + conv, 9x9 output conv.
+  segformer   SegFormer-B0 (artifact model P:743) at 512^2: MiT-b0 encoder
+              (C = 32/64/160/256, heads 1/2/5/8, sr 8/4/2/1, depth 2/2/2/2, MLP x4,
+              LN eps 1e-6, overlapping patch embeddings, Mix-FFN with 3x3 depthwise conv)
+              + all-MLP decoder (256 channels, 150 classes).  Token layout [1, HW, C];
+              the decoder's 1x1 convolutions are written as MatMuls on tokens and its
+              upsampling is nearest (the public model uses bilinear).
+BatchNorms are folded into the preceding conv at build time.
+"""
+from __future__ import annotations
+
+import math
+
+from .graphs import GraphBuilder
+
+
+class _M:
+    """Small helper around GraphBuilder that names weights automatically."""
+
+    def __init__(self, dtype):
+        self.b = GraphBuilder(dtype)
+        self.n = 0
+
+    def w(self, shape, std=None, mean=0.0):
+        self.n += 1
+        fan_in = 1
+        for d in shape[1:] if len(shape) > 1 else shape:
+            fan_in *= d
+        if std is None:
+            std = 1.0 / math.sqrt(max(1, fan_in))
+        return self.b.input(f"w{self.n}", shape, mean=mean, std=std)
+
+    def op(self, *a, **k):
+        return self.b.op(*a, **k)
+
+
+# ---------------------------------------------------------------------------------- Candy
+def candy(size: int = 224, dtype: str = "bf16", blocks: int = 5):
+    m = _M(dtype)
+    x = m.b.input("x", [1, 3, size, size])
+
+    def conv_layer(h, cin, cout, k, stride):
+        p = k // 2
+        h = m.op("Pad", h, pads=[[0, 0], [0, 0], [p, p], [p, p]], mode="reflect")
+        w = m.w([cout, cin, k, k], std=math.sqrt(2.0 / (cin * k * k)))
+        bias = m.w([cout], std=0.02)
+        return m.op("Conv", h, w, bias, stride=[stride, stride], pads=[0, 0], groups=1)
+
+    def inorm(h, c):
+        g = m.w([c], mean=1.0, std=0.1)
+        be = m.w([c], std=0.1)
+        return m.op("InstanceNorm", h, g, be, eps=1e-5)
+
+    h = m.op("Relu", inorm(conv_layer(x, 3, 32, 9, 1), 32))
+    h = m.op("Relu", inorm(conv_layer(h, 32, 64, 3, 2), 64))
+    h = m.op("Relu", inorm(conv_layer(h, 64, 128, 3, 2), 128))
+    for _ in range(blocks):
+        r = h
+        t = m.op("Relu", inorm(conv_layer(h, 128, 128, 3, 1), 128))
+        t = inorm(conv_layer(t, 128, 128, 3, 1), 128)
+        h = m.op("Add", t, r)
+    h = m.op("Upsample2x", h)
+    h = m.op("Relu", inorm(conv_layer(h, 128, 64, 3, 1), 64))
+    h = m.op("Upsample2x", h)
+    h = m.op("Relu", inorm(conv_layer(h, 64, 32, 3, 1), 32))
+    h = conv_layer(h, 32, 3, 9, 1)
+    m.b.output(h)
+    return m.b.build()
+
+
+# ------------------------------------------------------------------------------ SegFormer
+def segformer(size: int = 512, dtype: str = "bf16", dims=(32, 64, 160, 256), heads=(1, 2, 5, 8),
+              srs=(8, 4, 2, 1), depths=(2, 2, 2, 2), mlp=4, decoder=256, classes=150):
+    m = _M(dtype)
+    x = m.b.input("x", [1, 3, size, size])
+    eps = 1e-6
+
+    def ln(t, c):
+        g = m.w([c], mean=1.0, std=0.1)
+        be = m.w([c], std=0.1)
+        return m.op("LayerNorm", t, g, be, axis=-1, eps=eps)
+
+    def linear(t, cin, cout):
+        w = m.w([cin, cout])
+        b = m.w([cout], std=0.02)
+        return m.op("Add", m.op("MatMul", t, w), b)
+
+    def to_tokens(t, c, h, w):          # [1,C,H,W] -> [1,HW,C]
+        t = m.op("Reshape", t, shape=[1, c, h * w])
+        return m.op("Transpose", t, perm=[0, 2, 1])
+
+    def to_nchw(t, c, h, w):            # [1,HW,C] -> [1,C,H,W]
+        t = m.op("Transpose", t, perm=[0, 2, 1])
+        return m.op("Reshape", t, shape=[1, c, h, w])
+
+    feats = []
+    cur, cin, hw = x, 3, size
+    for s, (c, nh, sr, depth) in enumerate(zip(dims, heads, srs, depths)):
+        k, st = (7, 4) if s == 0 else (3, 2)
+        w = m.w([c, cin, k, k])
+        b = m.w([c], std=0.02)
+        t = m.op("Conv", cur, w, b, stride=[st, st], pads=[k // 2, k // 2], groups=1)
+        hw = hw // st
+        n = hw * hw
+        t = ln(to_tokens(t, c, hw, hw), c)
+        d = c // nh
+        for _ in range(depth):
+            # efficient self-attention with spatial reduction
+            y = ln(t, c)
+            q = linear(y, c, c)
+            if sr > 1:
+                kvx = to_nchw(y, c, hw, hw)
+                wr = m.w([c, c, sr, sr])
+                br = m.w([c], std=0.02)
+                kvx = m.op("Conv", kvx, wr, br, stride=[sr, sr], pads=[0, 0], groups=1)
+                nr = (hw // sr) ** 2
+                kvx = ln(to_tokens(kvx, c, hw // sr, hw // sr), c)
+            else:
+                kvx, nr = y, n
+            kv = linear(kvx, c, 2 * c)
+            qh = m.op("Transpose", m.op("Reshape", q, shape=[1, n, nh, d]), perm=[0, 2, 1, 3])
+            kk = m.op("Slice", kv, axis=2, start=0, end=c)
+            vv = m.op("Slice", kv, axis=2, start=c, end=2 * c)
+            kt = m.op("Transpose", m.op("Reshape", kk, shape=[1, nr, nh, d]), perm=[0, 2, 3, 1])
+            vh = m.op("Transpose", m.op("Reshape", vv, shape=[1, nr, nh, d]), perm=[0, 2, 1, 3])
+            sc = m.op("DivC", m.op("MatMul", qh, kt), c=math.sqrt(d))
+            p = m.op("Softmax", sc, axis=3)
+            o = m.op("MatMul", p, vh)
+            o = m.op("Reshape", m.op("Transpose", o, perm=[0, 2, 1, 3]), shape=[1, n, c])
+            t = m.op("Add", t, linear(o, c, c))
+            # Mix-FFN: fc1 -> 3x3 depthwise conv -> GELU -> fc2
+            y = ln(t, c)
+            y = linear(y, c, mlp * c)
+            y = to_nchw(y, mlp * c, hw, hw)
+            wd = m.w([mlp * c, 1, 3, 3], std=1.0 / 3.0)
+            bd = m.w([mlp * c], std=0.02)
+            y = m.op("Conv", y, wd, bd, stride=[1, 1], pads=[1, 1], groups=mlp * c)
+            y = m.op("GELU", to_tokens(y, mlp * c, hw, hw))
+            t = m.op("Add", t, linear(y, mlp * c, c))
+        t = ln(t, c)
+        feats.append((t, c, hw))
+        cur, cin = to_nchw(t, c, hw, hw), c
+    # all-MLP decoder: project every stage to `decoder` channels, upsample to 1/4, fuse
+    top = feats[0][2]
+    ups = []
+    for (t, c, hw) in reversed(feats):
+        u = linear(t, c, decoder)                                 # [1, hw*hw, D]
+        f = top // hw
+        if f > 1:                                                 # nearest x f in NHWC tokens
+            u = m.op("Reshape", u, shape=[1, hw, hw, decoder])
+            u = m.op("Broadcast", u, axis=2, size=f)
+            u = m.op("Broadcast", u, axis=4, size=f)
+            u = m.op("Reshape", u, shape=[1, top * top, decoder])
+        ups.append(u)
+    u = m.op("Concat", *ups, axis=2)                              # [1, top^2, 4D]
+    u = m.op("Relu", linear(u, 4 * decoder, decoder))             # linear_fuse (+folded BN) + ReLU
+    u = linear(u, decoder, classes)                               # linear_pred
+    m.b.output(u)
+    return m.b.build()
+
+
+MODELS = {"candy": candy, "segformer": segformer}

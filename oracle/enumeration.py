@@ -155,25 +155,48 @@ def candidates(g: PGraph, convex_sets, max_prims=16, prune_linear=True):
 
 
 def partition(g: PGraph, max_nodes: int = 64):
-    """Reading A17 (P:121 leaves the rule unspecified): cut only at articulation tensors.
+    """Reading A17 (P:121 leaves the rule unspecified): cut at articulation tensors.
 
     A cut may follow position i of the topological order (Kahn, smallest id first) when
-    exactly one primitive of the prefix topo[0..i] is consumed after it.  Parts are grown
-    greedily: when a part would exceed max_nodes it is closed at the latest cut inside
-    it; a part without any cut grows past max_nodes.  Returns lists of primitive ids."""
+    at most k primitives of the prefix topo[0..i] are consumed after it (they are
+    materialised).  k starts at 1 (single articulation tensors) and grows (up to 8) until
+    no part exceeds 2 * max_nodes.  Parts are grown greedily: when a part would exceed
+    max_nodes it is closed at the latest cut inside it.  Returns lists of primitive ids."""
+    for k in range(1, 9):
+        parts = _partition_k(g, max_nodes, k)
+        if max(len(p) for p in parts) <= 2 * max_nodes:
+            break
+    return parts
+
+
+def _partition_k(g: PGraph, max_nodes: int, max_cross: int):
     topo = g.topo
     n = len(topo)
     pos = {v: i for i, v in enumerate(topo)}
     last_use = [max((pos[w] for w in g.succs[v]), default=-1) for v in topo]
+    # cuts never split an operator's fission fragment (keeps operator-aligned kernels)
+    span = {}
+    for v in topo:
+        op = g.pg["nodes"][v].get("op")
+        op = ("p", v) if op is None or op < 0 else op
+        lo, hi = span.get(op, (n, -1))
+        span[op] = (min(lo, pos[v]), max(hi, pos[v]))
+    inside = [0] * (n + 1)
+    for lo, hi in span.values():
+        if hi > lo:
+            inside[lo] += 1
+            inside[hi] -= 1
     cut_after = []
     active = 0
+    open_ops = 0
     ends = [0] * (n + 1)
     for i, v in enumerate(topo):
         if last_use[i] > i:
             active += 1
             ends[last_use[i]] += 1
         active -= ends[i]
-        cut_after.append(active == 1 and i < n - 1)
+        open_ops += inside[i]
+        cut_after.append(1 <= active <= max_cross and i < n - 1 and open_ops == 0)
     parts, start, last_cut = [], 0, None
     for i in range(n):
         if i - start + 1 > max_nodes and last_cut is not None and last_cut >= start:

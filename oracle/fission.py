@@ -29,7 +29,7 @@ _SIMPLE = {"Exp": "exp", "Sqrt": "sqrt", "Erf": "erf", "Relu": "relu", "Sigmoid"
            "Tanh": "tanh", "Neg": "neg", "HardSwish": "hardswish", "Softplus": "softplus",
            "Identity": "identity", "AddC": "addc", "MulC": "mulc", "DivC": "divc",
            "Transpose": "transpose", "Reshape": "reshape", "Slice": "slice", "Pad": "pad",
-           "Concat": "concat", "MaxPool": "maxpool"}
+           "Concat": "concat", "MaxPool": "maxpool", "Broadcast": "broadcast"}
 _BIN = {"Add": "add", "Sub": "sub", "Mul": "mul", "Div": "div"}
 _RED = {"ReduceSum": "sum", "ReduceMean": "mean", "ReduceMax": "max"}
 

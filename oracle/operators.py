@@ -159,6 +159,8 @@ def eval_operator(kind: str, attrs: dict, args: list):
         return maxpool(args[0], attrs["k"], attrs["stride"], attrs.get("pad", 0))
     if kind == "Upsample2x":
         return np.repeat(np.repeat(args[0], 2, axis=2), 2, axis=3)
+    if kind == "Broadcast":
+        return np.repeat(np.expand_dims(args[0], attrs["axis"]), attrs["size"], axis=attrs["axis"])
     raise NotImplementedError(kind)
 
 

@@ -32,6 +32,7 @@ struct KernelVariant {
   int64_t grid_y = 1, grid_z = 1;
   int smem = 0;             // dynamic shared memory bytes
   int cluster = 1;
+  bool tcgen05 = false;     // source needs templates/sm100_gemm.cuh ahead of it
   int64_t scratch_bytes = 0;  // library-owned, zero-initialised, self-cleaning device scratch
                               // (split-K partial sums); passed right after `out`
   std::string tag;

@@ -10,6 +10,7 @@
 #include "enumerate.h"
 
 #include <algorithm>
+#include <map>
 #include <unordered_set>
 
 #include "../../include/korch.h"
@@ -51,21 +52,52 @@ struct Dfs {
 };
 }  // namespace
 
+static std::vector<std::vector<int>> partition_k(const Graph& g, int max_nodes, int max_cross);
+
+// Cuts where at most k tensors cross (all materialised), k = 1, 2, ... 8 until no part
+// exceeds 2 * max_nodes (reading A17).
 std::vector<std::vector<int>> partition_graph(const Graph& g, int max_nodes) {
+  std::vector<std::vector<int>> parts;
+  for (int k = 1; k <= 8; ++k) {
+    parts = partition_k(g, max_nodes, k);
+    size_t mx = 0;
+    for (auto& p : parts) mx = std::max(mx, p.size());
+    if ((int)mx <= 2 * max_nodes) break;
+  }
+  return parts;
+}
+
+static std::vector<std::vector<int>> partition_k(const Graph& g, int max_nodes, int max_cross) {
   int n = (int)g.prims.size();
   const std::vector<int>& topo = g.topo;
   std::vector<int> last_use(n, -1), ends(n + 1, 0);
   for (int i = 0; i < n; ++i)
     for (int w : g.succs[topo[i]]) last_use[i] = std::max(last_use[i], g.topo_index[w]);
+  // cuts never split an operator's fission fragment (keeps operator-aligned kernels)
+  std::map<long long, std::pair<int, int>> span;
+  for (int i = 0; i < n; ++i) {
+    int v = topo[i];
+    long long op = g.prims[v].op_id >= 0 ? (long long)g.prims[v].op_id : -1LL - v;
+    auto it = span.find(op);
+    if (it == span.end()) span[op] = {i, i};
+    else it->second = {std::min(it->second.first, i), std::max(it->second.second, i)};
+  }
+  std::vector<int> inside(n + 1, 0);
+  for (auto& kv : span)
+    if (kv.second.second > kv.second.first) {
+      ++inside[kv.second.first];
+      --inside[kv.second.second];
+    }
   std::vector<char> cut_after(n, 0);
-  int active = 0;
+  int active = 0, open_ops = 0;
   for (int i = 0; i < n; ++i) {
     if (last_use[i] > i) {
       ++active;
       ++ends[last_use[i]];
     }
     active -= ends[i];
-    cut_after[i] = active == 1 && i < n - 1;
+    open_ops += inside[i];
+    cut_after[i] = active >= 1 && active <= max_cross && i < n - 1 && open_ops == 0;
   }
   std::vector<std::vector<int>> parts;
   int start = 0, last_cut = -1;

@@ -404,13 +404,15 @@ KernelPlan generate_gemm(const Graph& g, const Candidate& c) {
     k << "  if (warp == 2) tc_dealloc(tmem, " << tcols << ");\n}\n";
 
     KernelVariant kv;
-    std::string src = std::string(kSm100GemmTemplate) + "\n" + k.str();
+    std::string src = k.str();
     char nm[64];
-    std::snprintf(nm, sizeof nm, "korch_gemm_%016llx", (unsigned long long)fnv1a(src));
+    std::snprintf(nm, sizeof nm, "korch_gemm_%016llx",
+                  (unsigned long long)fnv1a(std::string(kSm100GemmTemplate) + "\n" + src));
     kv.name = nm;
     size_t pos = src.find("KNAME");
     src.replace(pos, 5, kv.name);
     kv.source = src;
+    kv.tcgen05 = true;
     kv.block = 128;
     kv.grid = Mt;
     kv.grid_y = Nt;

@@ -343,7 +343,7 @@ Graph fission_graph(const Json& j) {
       {"HardSwish", Kind::HardSwish}, {"Softplus", Kind::Softplus}, {"Identity", Kind::Identity},
       {"AddC", Kind::AddC}, {"MulC", Kind::MulC}, {"DivC", Kind::DivC},
       {"Transpose", Kind::Transpose}, {"Reshape", Kind::Reshape}, {"Slice", Kind::Slice},
-      {"Pad", Kind::Pad}, {"Concat", Kind::Concat}, {"MaxPool", Kind::MaxPool}};
+      {"Pad", Kind::Pad}, {"Concat", Kind::Concat}, {"MaxPool", Kind::MaxPool}, {"Broadcast", Kind::Broadcast}};
   static const std::map<std::string, Kind> bins = {
       {"Add", Kind::Add}, {"Sub", Kind::Sub}, {"Mul", Kind::Mul}, {"Div", Kind::Div}};
   static const std::map<std::string, RedOp> reds = {

@@ -46,7 +46,7 @@ static korch_status fail(korch_status code, const std::string& msg) {
 
 // ------------------------------------------------------------------ compiled kernels
 struct Module {
-  std::string cubin;
+  std::shared_ptr<const std::string> cubin;  // shared by the kernels of one NVRTC batch
   std::string log;
   bool compiled = false, failed = false;
   CUmodule mod = nullptr;
@@ -69,6 +69,9 @@ struct korch_ctx {
   size_t flush_bytes = 0;
   std::mutex mu;
   std::map<std::string, std::unique_ptr<Module>> modules;  // kernel name -> module
+  std::map<const std::string*, CUmodule> loaded;           // batch cubin -> loaded module
+  std::map<std::string, int64_t> timings;                  // kernel + protocol -> ns
+  std::vector<std::shared_ptr<const std::string>> cubins;  // keeps loaded cubins alive
 
   void bind() {
     if (!gpu) throw KorchError(KORCH_E_CUDA, "host-only context (created with device -1)");
@@ -153,65 +156,124 @@ static void ensure_planned(korch_graph* G, int64_t i) {
   s.planned = true;
 }
 
-static std::string full_source(const KernelVariant& v) { return kernel_prelude() + v.source; }
+namespace korch {
+extern const char* kSm100GemmTemplate;
+}
 
-static bool compile_module(Module* m, const KernelVariant& v, const std::string& cache_dir) {
-  std::lock_guard<std::mutex> lk(m->mu);
-  if (m->compiled) return true;
-  if (m->failed) return false;
-  std::string path;
-  if (!cache_dir.empty()) {
-    path = cache_dir + "/" + v.name + ".cubin";
-    std::ifstream f(path, std::ios::binary);
-    if (f) {
-      std::stringstream ss;
-      ss << f.rdbuf();
-      m->cubin = ss.str();
-      if (!m->cubin.empty()) {
-        m->compiled = true;
-        return true;
-      }
-    }
-  }
+static std::string full_source(const KernelVariant& v) {
+  return kernel_prelude() + (v.tcgen05 ? std::string(kSm100GemmTemplate) + "\n" : std::string()) + v.source;
+}
+
+// Batched NVRTC compilation: up to kBatch kernels per program, so the per-program
+// overhead (front-end start-up, prelude and template parsing) is paid once per batch.
+// The batch cubin is shared by its kernels; the on-disk cache keeps one file per batch
+// plus one small "<kernel>.ref" file per kernel naming it.
+static constexpr size_t kBatch = 24;
+
+static std::mutex g_cubin_mu;
+static std::map<std::string, std::shared_ptr<const std::string>> g_cubin_files;  // path -> bytes
+
+static std::shared_ptr<const std::string> read_file_cached(const std::string& path) {
+  std::lock_guard<std::mutex> lk(g_cubin_mu);
+  auto it = g_cubin_files.find(path);
+  if (it != g_cubin_files.end()) return it->second;
+  std::ifstream f(path, std::ios::binary);
+  if (!f) return nullptr;
+  std::stringstream ss;
+  ss << f.rdbuf();
+  auto p = std::make_shared<const std::string>(ss.str());
+  if (p->empty()) return nullptr;
+  g_cubin_files[path] = p;
+  return p;
+}
+
+static bool cache_lookup(Module* m, const KernelVariant& v, const std::string& cache_dir) {
+  if (cache_dir.empty()) return false;
+  std::ifstream ref(cache_dir + "/" + v.name + ".ref");
+  if (!ref) return false;
+  std::string batch;
+  std::getline(ref, batch);
+  auto bytes = read_file_cached(cache_dir + "/" + batch);
+  if (!bytes) return false;
+  m->cubin = bytes;
+  m->compiled = true;
+  return true;
+}
+
+static bool nvrtc_compile(const std::string& src, const std::string& name, std::string* cubin, std::string* log) {
   NvrtcApi& nv = nvrtc();
   if (!nv.ok) {
-    m->failed = true;
-    m->log = nv.err;
+    *log = nv.err;
     return false;
   }
-  std::string src = full_source(v);
   nvrtcProgram prog;
-  if (nv.nvrtcCreateProgram(&prog, src.c_str(), (v.name + ".cu").c_str(), 0, nullptr, nullptr) != NVRTC_SUCCESS) {
-    m->failed = true;
-    m->log = "nvrtcCreateProgram failed";
+  if (nv.nvrtcCreateProgram(&prog, src.c_str(), (name + ".cu").c_str(), 0, nullptr, nullptr) != NVRTC_SUCCESS) {
+    *log = "nvrtcCreateProgram failed";
     return false;
   }
   const char* opts[] = {"-arch=sm_100a", "-std=c++17", "-default-device", "-lineinfo", "-DNDEBUG", "--diag-suppress=177,550"};
   nvrtcResult r = nv.nvrtcCompileProgram(prog, 6, opts);
   size_t ls = 0;
   nv.nvrtcGetProgramLogSize(prog, &ls);
-  std::string log(ls, '\0');
-  if (ls) nv.nvrtcGetProgramLog(prog, &log[0]);
+  std::string lg(ls, '\0');
+  if (ls) nv.nvrtcGetProgramLog(prog, &lg[0]);
   if (r != NVRTC_SUCCESS) {
-    m->failed = true;
-    m->log = std::string("NVRTC: ") + nv.nvrtcGetErrorString(r) + "\n" + log;
+    *log = std::string("NVRTC: ") + nv.nvrtcGetErrorString(r) + "\n" + lg;
     nv.nvrtcDestroyProgram(&prog);
     return false;
   }
   size_t cs = 0;
   nv.nvrtcGetCUBINSize(prog, &cs);
-  m->cubin.resize(cs);
-  nv.nvrtcGetCUBIN(prog, &m->cubin[0]);
+  cubin->resize(cs);
+  nv.nvrtcGetCUBIN(prog, &(*cubin)[0]);
   nv.nvrtcDestroyProgram(&prog);
-  m->compiled = true;
-  if (!path.empty()) {
-    std::string tmp = path + ".tmp" + std::to_string((uintptr_t)m);
-    std::ofstream f(tmp, std::ios::binary);
-    f.write(m->cubin.data(), (std::streamsize)m->cubin.size());
-    f.close();
-    std::rename(tmp.c_str(), path.c_str());
-  }
   return true;
+}
+
+static void write_atomic(const std::string& path, const std::string& data) {
+  std::string tmp = path + ".tmp" + std::to_string((uintptr_t)&data) + std::to_string(std::hash<std::thread::id>()(std::this_thread::get_id()));
+  {
+    std::ofstream f(tmp, std::ios::binary);
+    f.write(data.data(), (std::streamsize)data.size());
+  }
+  std::rename(tmp.c_str(), path.c_str());
+}
+
+// Compile one batch of kernels into a single cubin; on failure retry them one by one
+// so a bad kernel only rejects itself.
+static void compile_batch(const std::vector<std::pair<Module*, const KernelVariant*>>& jobs, const std::string& cache_dir) {
+  if (jobs.empty()) return;
+  bool tc = false;
+  std::string names;
+  for (auto& j : jobs) {
+    tc = tc || j.second->tcgen05;
+    names += j.second->name + ";";
+  }
+  std::string src = kernel_prelude() + (tc ? std::string(kSm100GemmTemplate) + "\n" : std::string());
+  for (auto& j : jobs) src += j.second->source + "\n";
+  char bname[64];
+  std::snprintf(bname, sizeof bname, "batch_%016llx.cubin", (unsigned long long)fnv1a(names + src));
+  std::string cubin, log;
+  if (nvrtc_compile(src, bname, &cubin, &log)) {
+    auto shared = std::make_shared<const std::string>(std::move(cubin));
+    if (!cache_dir.empty()) {
+      write_atomic(cache_dir + "/" + bname, *shared);
+      for (auto& j : jobs) write_atomic(cache_dir + "/" + j.second->name + ".ref", std::string(bname) + "\n");
+    }
+    for (auto& j : jobs) {
+      std::lock_guard<std::mutex> lk(j.first->mu);
+      j.first->cubin = shared;
+      j.first->compiled = true;
+    }
+    return;
+  }
+  if (jobs.size() == 1) {
+    std::lock_guard<std::mutex> lk(jobs[0].first->mu);
+    jobs[0].first->failed = true;
+    jobs[0].first->log = log;
+    return;
+  }
+  for (auto& j : jobs) compile_batch({j}, cache_dir);
 }
 
 static void compile_many(korch_graph* G, const std::vector<int64_t>& idx, int threads, const std::string& cache_dir) {
@@ -223,19 +285,34 @@ static void compile_many(korch_graph* G, const std::vector<int64_t>& idx, int th
     if (s.plan.klass == KORCH_CLASS_REJECTED) continue;
     for (auto& v : s.plan.variants) {
       Module* m = G->ctx->module_for(v.name);
-      if (m->compiled || m->failed || seen.count(m)) continue;
+      {
+        std::lock_guard<std::mutex> lk(m->mu);
+        if (m->compiled || m->failed || seen.count(m)) continue;
+        if (cache_lookup(m, v, cache_dir)) continue;
+      }
       seen[m] = true;
       jobs.push_back({m, &v});
     }
   }
+  // batches group kernels of one kind (tcgen05 kernels share the GEMM template)
+  std::stable_sort(jobs.begin(), jobs.end(), [](const std::pair<Module*, const KernelVariant*>& a,
+                                                const std::pair<Module*, const KernelVariant*>& b) {
+    return a.second->tcgen05 < b.second->tcgen05;
+  });
+  std::vector<std::vector<std::pair<Module*, const KernelVariant*>>> batches;
+  for (auto& j : jobs) {
+    if (batches.empty() || batches.back().size() >= kBatch || batches.back().back().second->tcgen05 != j.second->tcgen05)
+      batches.emplace_back();
+    batches.back().push_back(j);
+  }
   if (threads <= 0) threads = (int)std::max(1u, std::thread::hardware_concurrency());
-  threads = std::min<int>(threads, (int)std::max<size_t>(1, jobs.size()));
+  threads = std::min<int>(threads, (int)std::max<size_t>(1, batches.size()));
   std::atomic<size_t> next{0};
   auto worker = [&] {
     for (;;) {
       size_t k = next++;
-      if (k >= jobs.size()) break;
-      compile_module(jobs[k].first, *jobs[k].second, cache_dir);
+      if (k >= batches.size()) break;
+      compile_batch(batches[k], cache_dir);
     }
   };
   std::vector<std::thread> ts;
@@ -253,11 +330,20 @@ static CUfunction load_fn(korch_ctx* ctx, Module* m, const KernelVariant& v) {
   std::lock_guard<std::mutex> lk(m->mu);
   if (m->fn) return m->fn;
   if (!m->compiled) throw KorchError(KORCH_E_NVRTC, "kernel not compiled: " + m->log);
-  CU_CHECK(cuda().cuModuleLoadData(&m->mod, m->cubin.data()));
+  {
+    std::lock_guard<std::mutex> lk2(ctx->mu);
+    auto it = ctx->loaded.find(m->cubin.get());
+    if (it == ctx->loaded.end()) {
+      CUmodule mod;
+      CU_CHECK(cuda().cuModuleLoadData(&mod, m->cubin->data()));
+      it = ctx->loaded.emplace(m->cubin.get(), mod).first;
+      ctx->cubins.push_back(m->cubin);
+    }
+    m->mod = it->second;
+  }
   CU_CHECK(cuda().cuModuleGetFunction(&m->fn, m->mod, v.name.c_str()));
   if (v.smem > 48 * 1024)
     CU_CHECK(cuda().cuFuncSetAttribute(m->fn, CU_FUNC_ATTRIBUTE_MAX_DYNAMIC_SHARED_SIZE_BYTES, v.smem));
-  (void)ctx;
   return m->fn;
 }
 
@@ -383,10 +469,9 @@ korch_status korch_destroy(korch_ctx* c) {
   if (c->gpu && cuda().ok) {
     cuda().cuCtxSetCurrent(c->cuctx);
     cuda().cuCtxSynchronize();
-    for (auto& kv : c->modules) {
-      if (kv.second->mod) cuda().cuModuleUnload(kv.second->mod);
+    for (auto& kv : c->loaded) cuda().cuModuleUnload(kv.second);
+    for (auto& kv : c->modules)
       if (kv.second->scratch) cuda().cuMemFree(kv.second->scratch);
-    }
     if (c->arena) cuda().cuMemFree(c->arena);
     if (c->flush) cuda().cuMemFree(c->flush);
     if (c->pstream) cuda().cuStreamDestroy(c->pstream);
@@ -555,6 +640,34 @@ korch_status korch_profile(korch_graph* G, const int64_t* idx, int64_t n, const 
       CandState& s = G->cs[ci];
       cost[k] = INT64_MAX;
       if (s.plan.klass == KORCH_CLASS_REJECTED) { s.cost_ns = INT64_MAX; continue; }
+      // Candidates whose generated kernels are identical (same source => same shapes,
+      // strides and launch configuration) share one measurement.
+      int nv0 = tune ? (int)s.plan.variants.size() : 1;
+      auto tkey = [&](int vi) {
+        const KernelVariant& v = s.plan.variants[vi];
+        return v.name + "|" + std::to_string(flush) + "|" + std::to_string(flush ? 1 : launches) + "|" +
+               std::to_string(trials);
+      };
+      {
+        bool all_cached = true;
+        std::lock_guard<std::mutex> lk(ctx->mu);
+        for (int vi = 0; vi < nv0 && all_cached; ++vi)
+          if (!ctx->timings.count(tkey(vi))) all_cached = false;
+        if (all_cached) {
+          s.var_ns.assign(s.plan.variants.size(), -1);
+          int64_t best = INT64_MAX;
+          int bestv = -1;
+          for (int vi = 0; vi < nv0; ++vi) {
+            int64_t ns = ctx->timings[tkey(vi)];
+            s.var_ns[vi] = ns;
+            if (ns < best) { best = ns; bestv = vi; }
+          }
+          s.best = bestv;
+          s.cost_ns = best;
+          cost[k] = best;
+          continue;
+        }
+      }
       // scratch buffers at the candidate's exact shapes
       std::vector<size_t> offs;
       size_t tot = 0;
@@ -616,6 +729,10 @@ korch_status korch_profile(korch_graph* G, const int64_t* idx, int64_t n, const 
           int64_t ns = (int64_t)std::llround((double)ts[ts.size() / 2] * 1e6);
           if (ns < 1) ns = 1;
           s.var_ns[vi] = ns;
+          {
+            std::lock_guard<std::mutex> lk(ctx->mu);
+            ctx->timings[tkey(vi)] = ns;
+          }
           if (ns < best) { best = ns; bestv = vi; }
         } catch (KorchError& e) {
           // a variant that fails to launch is rejected (cost = inf for it)

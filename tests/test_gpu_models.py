@@ -1,0 +1,68 @@
+"""Whole paper models through the C ABI at reduced sizes: Candy (IN/ReLU/pad
+CNN) and SegFormer (LN/attention transformer), partitioned (reading A17), executed with
+the operator-aligned orchestration and with a BLP-selected orchestration over profiled
+candidates; outputs against the oracle's orchestration-aware fp64 evaluation of the
+same orchestration (bf16 storage, rtol 2e-2 of the output's max norm)."""
+import numpy as np
+import pytest
+
+from korch_workloads import make_inputs
+from korch_workloads.models import candy, segformer
+from oracle.enumeration import PGraph
+from oracle.evaluate import eval_orchestration
+from oracle.fission import fission
+
+torch = pytest.importorskip("torch")
+
+
+@pytest.fixture(scope="module")
+def ctx():
+    from paper_2406_09465_b200 import Context
+    return Context(0)
+
+
+def _run_and_check(ctx, graph, max_members=2, rtol=2e-2):
+    from paper_2406_09465_b200 import KorchGraph, torch_inputs
+    kg = KorchGraph(ctx, graph)
+    cands = kg.enumerate(partition_max=64)
+    pg = fission(graph)
+    G = PGraph(pg)
+    ref_cands = [(tuple(c["members"]), c["output"]) for c in cands]
+    ins = make_inputs(graph, seed=0)
+    vals = {k: v[0] for k, v in ins.items()}
+    dev = torch_inputs(graph, {k: v[1] for k, v in ins.items()})
+    small = [c["index"] for c in cands if len(c["members"]) <= max_members and c["klass"] != "rejected"]
+    base = kg.operator_aligned()
+    prof = sorted(set(small) | set(base))
+    costs = [(1 << 63) - 1] * len(cands)
+    for i, ns in zip(prof, kg.profile(prof)):
+        costs[i] = ns
+    obj, sel = kg.select(costs)
+    assert obj <= sum(costs[i] for i in base)
+    for orch in (base, sel):
+        kg.set_orchestration(orch)
+        outs, ws = kg.torch_outputs(), kg.torch_workspace()
+        kg.execute(dev, outs, ws, torch.cuda.current_stream())
+        torch.cuda.synchronize()
+        want = eval_orchestration(pg, ref_cands, orch, vals, G.topo_index, graph["dtype"])
+        for k, o in enumerate(kg.outputs):
+            got = outs[k].float().cpu().numpy().astype(np.float64)
+            r = want[o]
+            assert np.isfinite(got).all()
+            err = np.max(np.abs(got - r)) / np.max(np.abs(r))
+            assert err <= rtol, f"rel err {err:.3e}"
+    return len(cands), len(sel), len(base)
+
+
+@pytest.mark.gpu
+@pytest.mark.timeout(1200)
+def test_candy_small(ctx):
+    n, k_sel, k_base = _run_and_check(ctx, candy(size=32, blocks=1))
+    assert n > 500 and k_sel < k_base
+
+
+@pytest.mark.gpu
+@pytest.mark.timeout(1200)
+def test_segformer_small(ctx):
+    n, k_sel, k_base = _run_and_check(ctx, segformer(size=64, depths=(1, 1, 1, 1)))
+    assert n > 1000 and k_sel < k_base

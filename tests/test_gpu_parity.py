@@ -178,6 +178,49 @@ def test_misc_memory_bound_ops(ctx):
     c.check(c.kg.operator_aligned())
 
 
+def _cnn_graph(dtype="bf16"):
+    b = GraphBuilder(dtype)
+    x = b.input("x", [1, 16, 20, 24])
+    w = b.input("w", [32, 16, 3, 3], std=0.08)
+    bias = b.input("bias", [32], std=0.1)
+    y = b.op("Conv", x, w, bias, stride=[1, 1], pads=[1, 1], groups=1)
+    y = b.op("SiLU", y)
+    y = b.op("MaxPool", y, k=3, stride=2, pad=1)                      # [1,32,10,12]
+    dw = b.input("dw", [32, 1, 3, 3], std=0.3)
+    z = b.op("Conv", y, dw, stride=[2, 2], pads=[1, 1], groups=32)    # depthwise, stride 2
+    z = b.op("HardSwish", z)
+    pw = b.input("pw", [24, 32, 1, 1], std=0.2)
+    z = b.op("Conv", z, pw, stride=[1, 1], pads=[0, 0], groups=1)     # pointwise
+    z = b.op("Upsample2x", z)                                          # [1,24,10,12]
+    y2 = b.op("Slice", y, axis=1, start=0, end=8)
+    c = b.op("Concat", z, y2, axis=1)                                  # [1,32,10,12]
+    g = b.input("g", [32], mean=1.0, std=0.1)
+    be = b.input("be", [32], std=0.1)
+    c = b.op("InstanceNorm", c, g, be, eps=1e-5)
+    c = b.op("Relu", c)
+    c = b.op("Pad", c, pads=[[0, 0], [0, 0], [1, 1], [1, 1]], mode="reflect")
+    w3 = b.input("w3", [3, 32, 3, 3], std=0.05)
+    c = b.op("Conv", c, w3, stride=[1, 1], pads=[0, 0], groups=1)
+    b.output(c)
+    return b.build()
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("dtype", ["bf16", "f32"])
+def test_cnn_primitives(ctx, dtype):
+    """Dense / depthwise / strided / pointwise convolutions (+bias), max-pool, concat,
+    slice, upsample, InstanceNorm, reflect pad, SiLU, HardSwish: every generable
+    candidate inside a feasible orchestration, then the BLP plan."""
+    c = Case(ctx, _cnn_graph(dtype))
+    gen = [x["index"] for x in c.cands if x["klass"] != "rejected"]
+    assert len(gen) > 50
+    for i in gen:
+        c.check(c.completion([i]))
+    costs = c.kg.profile()
+    obj, sel = c.kg.select(costs)
+    c.check(sel)
+
+
 @pytest.mark.gpu
 def test_c2_every_gemm_candidate(ctx):
     """Every tcgen05 GEMM candidate of the ViT attention layer (fused views + epilogues)."""

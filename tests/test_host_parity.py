@@ -62,6 +62,12 @@ def _rw(g):
     return g
 
 
+def _cnn():
+    from test_gpu_parity import _cnn_graph
+    return _cnn_graph()
+
+
+GRAPHS["cnn"] = _cnn
 GRAPHS["c2_r1r3"] = lambda: _rw(c2_vit_attention())
 GRAPHS["c2_b2_r1r3"] = lambda: _rw(c2_vit_attention(batch=2, seq=32, hidden=128, heads=4))
 
