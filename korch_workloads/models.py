@@ -164,4 +164,80 @@ def segformer(size: int = 512, dtype: str = "bf16", dims=(32, 64, 160, 256), hea
     return m.b.build()
 
 
-MODELS = {"candy": candy, "segformer": segformer}
+# --------------------------------------------------------------------------- EfficientViT
+def efficientvit(size: int = 224, dtype: str = "bf16", widths=(16, 32, 64, 128, 256), depths=(1, 2, 3, 3, 4),
+                 dim: int = 16, expand: int = 4, eps: float = 1e-15):
+    """EfficientViT-B1 backbone: conv stem + DSConv, MBConv
+    stages, then EfficientViT blocks (LiteMLA ReLU linear attention with 5x5 multi-scale
+    aggregation + MBConv).  Hardswish activations, BN folded.  Pointwise (1x1) convs are
+    MatMuls over [C, HW] (tcgen05 GEMMs); depthwise / strided convs stay Conv."""
+    m = _M(dtype)
+    x = m.b.input("x", [1, 3, size, size])
+
+    def conv(h, cin, cout, k, stride=1, groups=1, bias=True):
+        w = m.w([cout, cin // groups, k, k])
+        args = [h, w] + ([m.w([cout], std=0.02)] if bias else [])
+        return m.op("Conv", *args, stride=[stride, stride], pads=[k // 2, k // 2], groups=groups)
+
+    def pw(h, cin, cout, hw, bias=True):             # 1x1 conv as MatMul on [C, HW]
+        t = m.op("Reshape", h, shape=[cin, hw * hw])
+        t = m.op("MatMul", m.w([cout, cin]), t)
+        if bias:
+            t = m.op("Add", t, m.w([cout, 1], std=0.02))
+        return m.op("Reshape", t, shape=[1, cout, hw, hw])
+
+    def mbconv(h, cin, cout, hw, stride, act_last=False):
+        mid = cin * expand
+        t = m.op("HardSwish", pw(h, cin, mid, hw))
+        t = m.op("HardSwish", conv(t, mid, mid, 3, stride, groups=mid))
+        hw2 = hw // stride
+        t = pw(t, mid, cout, hw2)
+        return (m.op("HardSwish", t) if act_last else t), hw2
+
+    def lite_mla(h, c, hw):
+        heads = c // dim
+        n = hw * hw
+        qkv = pw(h, c, 3 * c, hw, bias=False)                                        # [1,3c,hw,hw]
+        agg = conv(qkv, 3 * c, 3 * c, 5, groups=3 * c, bias=False)                   # 5x5 depthwise
+        agg = conv(agg, 3 * c, 3 * c, 1, groups=3 * heads, bias=False)               # grouped 1x1
+        ms = m.op("Concat", qkv, agg, axis=1)                                        # [1,6c,hw,hw]
+        ms = m.op("Reshape", ms, shape=[1, 2 * heads, 3 * dim, n])
+        ms = m.op("Transpose", ms, perm=[0, 1, 3, 2])                                # [1,2h,n,3d]
+        q = m.op("Relu", m.op("Slice", ms, axis=3, start=0, end=dim))
+        k = m.op("Relu", m.op("Slice", ms, axis=3, start=dim, end=2 * dim))
+        v = m.op("Slice", ms, axis=3, start=2 * dim, end=3 * dim)
+        v = m.op("Pad", v, pads=[[0, 0], [0, 0], [0, 0], [0, 1]], mode="constant", value=1.0)
+        kt = m.op("Transpose", k, perm=[0, 1, 3, 2])                                 # [1,2h,d,n]
+        kv = m.op("MatMul", kt, v)                                                   # [1,2h,d,d+1]
+        o = m.op("MatMul", q, kv)                                                    # [1,2h,n,d+1]
+        num = m.op("Slice", o, axis=3, start=0, end=dim)
+        den = m.op("AddC", m.op("Slice", o, axis=3, start=dim, end=dim + 1), c=eps)
+        den = m.op("Reshape", den, shape=[1, 2 * heads, n])
+        o = m.op("Div", num, m.op("Broadcast", den, axis=3, size=dim))
+        o = m.op("Transpose", o, perm=[0, 1, 3, 2])                                  # [1,2h,d,n]
+        o = m.op("Reshape", o, shape=[1, 2 * c, hw, hw])
+        return pw(o, 2 * c, c, hw)
+
+    h = m.op("HardSwish", conv(x, 3, widths[0], 3, 2))
+    hw = size // 2
+    for _ in range(depths[0]):                                                       # DSConv + residual
+        t = m.op("HardSwish", conv(h, widths[0], widths[0], 3, groups=widths[0]))
+        h = m.op("Add", h, pw(t, widths[0], widths[0], hw))
+    cin = widths[0]
+    for w, d in zip(widths[1:3], depths[1:3]):
+        for i in range(d):
+            t, hw2 = mbconv(h, cin, w, hw, 2 if i == 0 else 1)
+            h = t if i == 0 else m.op("Add", h, t)
+            hw, cin = hw2, w
+    for w, d in zip(widths[3:], depths[3:]):
+        h, hw = mbconv(h, cin, w, hw, 2)
+        cin = w
+        for _ in range(d):
+            h = m.op("Add", h, lite_mla(h, w, hw))
+            t, _ = mbconv(h, w, w, hw, 1)
+            h = m.op("Add", h, t)
+    m.b.output(h)
+    return m.b.build()
+
+
+MODELS = {"candy": candy, "segformer": segformer, "efficientvit": efficientvit}

@@ -202,6 +202,27 @@ def test_partitioned_blp_equals_global_optimum(ctx):
         assert feasible(ref, sel, G.pg["outputs"], cin)
 
 
+@pytest.mark.parametrize("name", ["efficientvit", "candy", "segformer"])
+def test_models_fission_and_partitioned_enumeration(ctx, name):
+    """Whole paper models (reduced sizes): primitive graph and partitioned candidate list
+    bit-identical to the oracle's."""
+    from korch_workloads.models import candy, efficientvit, segformer
+    from oracle.enumeration import candidates_partitioned, partition
+    g = {"efficientvit": lambda: efficientvit(size=32, depths=(1, 1, 1, 1, 1)),
+         "candy": lambda: candy(size=16, blocks=1),
+         "segformer": lambda: segformer(size=32, depths=(1, 1, 1, 1))}[name]()
+    kg = KorchGraph(ctx, g)
+    ref_pg = fission(g)
+    assert [(n["kind"], tuple(n["shape"])) for n in kg.prim["nodes"]] == \
+        [(n["kind"], tuple(n["shape"])) for n in ref_pg["nodes"]]
+    ours = kg.enumerate(partition_max=32)
+    G = PGraph(ref_pg)
+    ref, n_states = candidates_partitioned(G, partition(G, 32))
+    assert [(tuple(c["members"]), c["output"]) for c in ours] == [(tuple(m), o) for m, o in ref]
+    assert kg.n_states == n_states
+    assert len(kg.operator_aligned()) == len(g["nodes"])
+
+
 def test_blp_with_rejections_and_baselines(ctx):
     g = c2_vit_attention()
     kg = KorchGraph(ctx, g)
