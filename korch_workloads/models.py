@@ -240,4 +240,95 @@ def efficientvit(size: int = 224, dtype: str = "bf16", widths=(16, 32, 64, 128, 
     return m.b.build()
 
 
-MODELS = {"candy": candy, "segformer": segformer, "efficientvit": efficientvit}
+# ----------------------------------------------------------------------------- YOLOX-Nano
+def yolox_nano(size: int = 416, dtype: str = "bf16", width: float = 0.25, classes: int = 80):
+    """YOLOX-Nano: Focus, depthwise CSPDarknet (depth 0.33,
+    width 0.25), SPP 5/9/13, PAFPN, decoupled heads; SiLU, BN folded.  Output
+    [1, 3549, 85] at 416^2 = cat(reg, sigmoid(obj), sigmoid(cls)) per anchor point (the box
+    decode with grids / strides is not part of the graph).  1x1 convs are MatMuls over
+    [C, HW]; depthwise and 3x3 convs stay Conv."""
+    m = _M(dtype)
+    x = m.b.input("x", [1, 3, size, size])
+    c0 = int(64 * width)
+
+    def silu(h):
+        return m.op("SiLU", h)
+
+    def pw(h, cin, cout, hw):                       # BaseConv 1x1 + SiLU as a MatMul
+        t = m.op("Reshape", h, shape=[cin, hw * hw])
+        t = m.op("Add", m.op("MatMul", m.w([cout, cin]), t), m.w([cout, 1], std=0.02))
+        return silu(m.op("Reshape", t, shape=[1, cout, hw, hw]))
+
+    def conv(h, cin, cout, k, stride, groups=1):
+        t = m.op("Conv", h, m.w([cout, cin // groups, k, k]), m.w([cout], std=0.02),
+                 stride=[stride, stride], pads=[k // 2, k // 2], groups=groups)
+        return silu(t)
+
+    def dwconv(h, cin, cout, hw, stride=1):         # depthwise 3x3 + pointwise 1x1
+        t = conv(h, cin, cin, 3, stride, groups=cin)
+        return pw(t, cin, cout, hw // stride), hw // stride
+
+    def csp(h, cin, cout, hw, n, shortcut=True):
+        hid = cout // 2
+        x1 = pw(h, cin, hid, hw)
+        for _ in range(n):
+            y = pw(x1, hid, hid, hw)
+            y, _ = dwconv(y, hid, hid, hw)
+            x1 = m.op("Add", y, x1) if shortcut else y
+        x2 = pw(h, cin, hid, hw)
+        return pw(m.op("Concat", x1, x2, axis=1), 2 * hid, cout, hw)
+
+    # Focus: space-to-depth, channel order (w-parity, h-parity, c)
+    hw = size // 2
+    f = m.op("Reshape", x, shape=[1, 3, hw, 2, hw, 2])
+    f = m.op("Transpose", f, perm=[0, 5, 3, 1, 2, 4])
+    f = m.op("Reshape", f, shape=[1, 12, hw, hw])
+    h = conv(f, 12, c0, 3, 1)
+    h, hw = dwconv(h, c0, 2 * c0, hw, 2)
+    h = csp(h, 2 * c0, 2 * c0, hw, 1)
+    h, hw = dwconv(h, 2 * c0, 4 * c0, hw, 2)
+    x2 = csp(h, 4 * c0, 4 * c0, hw, 1)                                      # 52^2, 64
+    h, hw1 = dwconv(x2, 4 * c0, 8 * c0, hw, 2)
+    x1 = csp(h, 8 * c0, 8 * c0, hw1, 1)                                     # 26^2, 128
+    h, hw0 = dwconv(x1, 8 * c0, 16 * c0, hw1, 2)
+    sp = pw(h, 16 * c0, 8 * c0, hw0)                                        # SPP
+    pools = [m.op("MaxPool", sp, k=k, stride=1, pad=k // 2) for k in (5, 9, 13)]
+    h = pw(m.op("Concat", sp, *pools, axis=1), 32 * c0, 16 * c0, hw0)
+    x0 = csp(h, 16 * c0, 16 * c0, hw0, 1, shortcut=False)                  # 13^2, 256
+    # PAFPN
+    fpn0 = pw(x0, 16 * c0, 8 * c0, hw0)
+    u = m.op("Concat", m.op("Upsample2x", fpn0), x1, axis=1)
+    u = csp(u, 16 * c0, 8 * c0, hw1, 1, shortcut=False)
+    fpn1 = pw(u, 8 * c0, 4 * c0, hw1)
+    u = m.op("Concat", m.op("Upsample2x", fpn1), x2, axis=1)
+    pan2 = csp(u, 8 * c0, 4 * c0, hw, 1, shortcut=False)                   # 52^2, 64
+    d, _ = dwconv(pan2, 4 * c0, 4 * c0, hw, 2)
+    pan1 = csp(m.op("Concat", d, fpn1, axis=1), 8 * c0, 8 * c0, hw1, 1, shortcut=False)
+    d, _ = dwconv(pan1, 8 * c0, 8 * c0, hw1, 2)
+    pan0 = csp(m.op("Concat", d, fpn0, axis=1), 16 * c0, 16 * c0, hw0, 1, shortcut=False)
+    # decoupled heads
+    hid = int(256 * width)
+    outs = []
+    for feat, cin, s in ((pan2, 4 * c0, hw), (pan1, 8 * c0, hw1), (pan0, 16 * c0, hw0)):
+        st = pw(feat, cin, hid, s)
+        c, _ = dwconv(st, hid, hid, s)
+        c, _ = dwconv(c, hid, hid, s)
+        r, _ = dwconv(st, hid, hid, s)
+        r, _ = dwconv(r, hid, hid, s)
+
+        def pred(t, cout):
+            t2 = m.op("Reshape", t, shape=[hid, s * s])
+            return m.op("Add", m.op("MatMul", m.w([cout, hid]), t2), m.w([cout, 1], std=0.02))   # [cout, s*s]
+        o = m.op("Concat", pred(r, 4), m.op("Sigmoid", pred(r, 1)), m.op("Sigmoid", pred(c, classes)), axis=0)
+        outs.append(o)                                                                           # [85, s*s]
+    o = m.op("Concat", *outs, axis=1)                                                            # [85, 3549]
+    o = m.op("Transpose", o, perm=[1, 0])
+    m.b.output(m.op("Reshape", o, shape=[1, o_n(size), 5 + classes]))
+    return m.b.build()
+
+
+def o_n(size):
+    return sum((size // s) ** 2 for s in (8, 16, 32))
+
+
+MODELS = {"candy": candy, "segformer": segformer, "efficientvit": efficientvit, "yolox": yolox_nano}

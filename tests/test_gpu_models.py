@@ -71,6 +71,14 @@ def test_efficientvit_small(ctx):
 
 @pytest.mark.gpu
 @pytest.mark.timeout(1200)
+def test_yolox_small(ctx):
+    from korch_workloads.models import yolox_nano
+    n, k_sel, k_base = _run_and_check(ctx, yolox_nano(size=64))
+    assert n > 1000 and k_sel < k_base
+
+
+@pytest.mark.gpu
+@pytest.mark.timeout(1200)
 def test_segformer_small(ctx):
     n, k_sel, k_base = _run_and_check(ctx, segformer(size=64, depths=(1, 1, 1, 1)))
     assert n > 1000 and k_sel < k_base

@@ -202,15 +202,16 @@ def test_partitioned_blp_equals_global_optimum(ctx):
         assert feasible(ref, sel, G.pg["outputs"], cin)
 
 
-@pytest.mark.parametrize("name", ["efficientvit", "candy", "segformer"])
+@pytest.mark.parametrize("name", ["efficientvit", "candy", "segformer", "yolox"])
 def test_models_fission_and_partitioned_enumeration(ctx, name):
     """Whole paper models (reduced sizes): primitive graph and partitioned candidate list
     bit-identical to the oracle's."""
-    from korch_workloads.models import candy, efficientvit, segformer
+    from korch_workloads.models import candy, efficientvit, segformer, yolox_nano
     from oracle.enumeration import candidates_partitioned, partition
     g = {"efficientvit": lambda: efficientvit(size=32, depths=(1, 1, 1, 1, 1)),
          "candy": lambda: candy(size=16, blocks=1),
-         "segformer": lambda: segformer(size=32, depths=(1, 1, 1, 1))}[name]()
+         "segformer": lambda: segformer(size=32, depths=(1, 1, 1, 1)),
+         "yolox": lambda: yolox_nano(size=64)}[name]()
     kg = KorchGraph(ctx, g)
     ref_pg = fission(g)
     assert [(n["kind"], tuple(n["shape"])) for n in kg.prim["nodes"]] == \
