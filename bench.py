@@ -162,6 +162,9 @@ def time_plan(kg, sel, dev_in, steps=20, flush_mb=512):
     return statistics.mean(a.elapsed_time(e) for a, e in ev), outs
 
 
+MODEL_MAX_PRIMS = 12  # SPEC S:393's default; whole models only (reading A5)
+
+
 def run_models(K, names, oracle_check=True):
     """Whole paper models at their paper input sizes, bs = 1: partition,
     enumerate, compile, profile, BLP-select, then measure the chosen orchestration and the
@@ -170,7 +173,8 @@ def run_models(K, names, oracle_check=True):
     import torch
     from korch_workloads import make_inputs
     from korch_workloads.models import MODELS
-    os.environ["KORCH_CACHE_DIR"] = os.environ.get("KORCH_MODEL_CACHE", "/tmp/korch_model_cache")
+    os.environ["KORCH_CACHE_DIR"] = os.environ.get(
+        "KORCH_MODEL_CACHE", os.path.join(ROOT, "paper_2406_09465_b200", "kcache_models"))
     os.makedirs(os.environ["KORCH_CACHE_DIR"], exist_ok=True)
     res = {}
     for name in names:
@@ -178,7 +182,7 @@ def run_models(K, names, oracle_check=True):
         graph = MODELS[name]()
         ctx = K.Context(torch.cuda.current_device())
         kg = K.KorchGraph(ctx, graph)
-        cands = kg.enumerate(partition_max=64)
+        cands = kg.enumerate(partition_max=64, max_prims=MODEL_MAX_PRIMS)
         t_enum = time.perf_counter() - t0
         t1 = time.perf_counter()
         kg.compile()

@@ -100,6 +100,186 @@ std::string str(int64_t v) { return std::to_string(v); }
 
 }  // namespace
 
+// KB6: implicit-GEMM convolution on tcgen05.  D[f, p] = sum_k W[f, k] * X_col[k, p] with
+// f = output channel, p = output pixel (n, oh, ow) linearised, k = (c, r, s) in the weight's
+// natural [F, C, R, S] order.  A (weights) streams by TMA (K-major, 128B swizzle); the
+// im2col operand B is gathered by four producer warps straight from the NCHW input into
+// the canonical MN-major 128B-swizzled shared-memory layout (zero padding, strides and the
+// K tail as predicated loads), published to the tensor core with fence.proxy.async and an
+// mbarrier; one thread issues the MMAs; the fused epilogue is the GEMM template's.
+static KernelPlan generate_conv_gemm(const Graph& g, const Candidate& c, int mm) {
+  KernelPlan kp;
+  kp.klass = KORCH_CLASS_REJECTED;
+  const Prim& L = g.prims[mm];
+  std::set<int> mem(c.members.begin(), c.members.end());
+  for (int m : c.members)
+    for (int p : g.preds[m])
+      if (m == mm && mem.count(p)) {
+        kp.reject = "conv operand computed inside the candidate";
+        return kp;
+      }
+  const Ref& xr = L.in[0];
+  const Ref& wr = L.in[1];
+  if (!xr.is_input && mem.count(xr.id)) { kp.reject = "conv input computed inside the candidate"; return kp; }
+  if (g.dtype_of(xr) != DType::BF16 || g.dtype_of(wr) != DType::BF16) {
+    kp.reject = "conv operands must be bf16";
+    return kp;
+  }
+  if (L.groups != 1) { kp.reject = "grouped convolution"; return kp; }
+  const Shape& xs = g.shape_of(xr);
+  const Shape& ws = g.shape_of(wr);
+  const Shape& ys = L.shape;
+  int64_t Cin = xs[1], H = xs[2], W = xs[3], F = ws[0], R = ws[2], S = ws[3];
+  int64_t K = Cin * R * S, OH = ys[2], OW = ys[3], NP = ys[0] * OH * OW;
+  if (K % 8) { kp.reject = "conv K = C*R*S not a multiple of 8 (TMA row stride)"; return kp; }
+  std::vector<Ref> pre{wr, xr};
+  GemmEpilogue ep0;
+  std::string err;
+  if (!make_gemm_epilogue(g, c, mm, 32, pre, &ep0, &err)) {
+    kp.reject = err;
+    return kp;
+  }
+  kp.ext = ep0.ext;
+  const int slotW = 0, slotX = 1;
+  kp.flops = 2.0 * (double)F * (double)NP * (double)K;
+  kp.bytes = ep0.bytes + 2 * (F * K + numel(xs));
+  const int64_t NK = (K + 63) / 64, Mt = (F + 127) / 128;
+  for (int BN : {64, 128}) {
+    GemmEpilogue ep;
+    if (!make_gemm_epilogue(g, c, mm, 32, pre, &ep, &err)) continue;
+    const int A_BYTES = 128 * 64 * 2, B_BYTES = BN * 64 * 2, STAGE = A_BYTES + B_BYTES;
+    const int S_ = (int)std::max<int64_t>(2, std::min<int64_t>({NK, 4, (200 * 1024) / STAGE}));
+    const int smem = S_ * STAGE + 1024 + (2 * S_ + 1) * 8 + 16;
+    const int64_t Nt = (NP + BN - 1) / BN;
+    const int tcols = BN;
+    const uint32_t idesc = (1u << 4) | (1u << 7) | (1u << 10) | (0u << 15) | (1u << 16) |
+                           ((uint32_t)(BN >> 3) << 17) | ((uint32_t)(128 >> 4) << 24);
+    TmaDesc da;
+    da.tensor = slotW;
+    da.dtype = 1;
+    da.swizzle = 3;
+    da.elem_off = 0;
+    da.rank = 2;
+    da.dims[0] = K; da.strides[0] = 2; da.box[0] = 64;
+    da.dims[1] = F; da.strides[1] = K * 2; da.box[1] = 128;
+    std::ostringstream k;
+    k << "extern \"C\" __global__ void __launch_bounds__(192, 1) KNAME(";
+    for (size_t i = 0; i < kp.ext.size(); ++i)
+      k << "const " << (g.dtype_of(kp.ext[i]) == DType::F32 ? "float" : "bf16_t") << "* __restrict__ p" << i << ", ";
+    k << (g.prims[c.output].dtype == DType::F32 ? "float" : "bf16_t") << "* __restrict__ out, "
+      << "const __grid_constant__ TmaMap tmA) {\n";
+    k << "  typedef int idx_t;\n";
+    k << "  extern __shared__ __align__(1024) unsigned char smem_raw[];\n";
+    k << "  unsigned char* smem = (unsigned char*)(((unsigned long long)smem_raw + 1023ull) & ~1023ull);\n";
+    k << "  unsigned long long* full = (unsigned long long*)(smem + " << S_ * STAGE << ");\n";
+    k << "  unsigned long long* empty = full + " << S_ << ";\n";
+    k << "  unsigned long long* accf = empty + " << S_ << ";\n";
+    k << "  unsigned* tslot = (unsigned*)(accf + 1);\n";
+    k << "  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;\n";
+    k << "  const int tile_m = blockIdx.x * 128, tile_n = blockIdx.y * " << BN << ";\n";
+    k << "  if (threadIdx.x == 0) {\n    for (int s = 0; s < " << S_
+      << "; ++s) { mbar_init(full + s, 5); mbar_init(empty + s, 1); }\n"
+      << "    mbar_init(accf, 1);\n    mbar_fence_init();\n    tma_prefetch(&tmA);\n  }\n";
+    k << "  if (warp == 5) tc_alloc(tslot, " << tcols << ");\n";
+    k << "  tc_fence_before();\n  __syncthreads();\n  tc_fence_after();\n";
+    k << "  const unsigned tmem = *tslot;\n";
+    k << "  pdl_trigger();\n  pdl_wait();\n";
+    // gather producers: warps 0-3
+    k << "  if (warp < 4) {\n";
+    k << "    const bf16_t* __restrict__ xin = p" << slotX << ";\n";
+    k << "    int s = 0; unsigned ph = 0;\n";
+    k << "    for (int kb = 0; kb < " << NK << "; ++kb) {\n";
+    k << "      mbar_wait(empty + s, ph ^ 1u);\n";
+    k << "      const unsigned sb = smem_u32(smem + s * " << STAGE << " + " << A_BYTES << ");\n";
+    k << "      for (int u = threadIdx.x; u < " << 64 * (BN / 8) << "; u += 128) {\n";
+    k << "        const int kk = u / " << BN / 8 << ", grp = u % " << BN / 8 << ";\n";
+    k << "        const int kg = kb * 64 + kk;\n";
+    k << "        const int ci = kg / " << R * S << ", rs = kg % " << R * S << ";\n";
+    k << "        const int rr = rs / " << S << ", ss = rs % " << S << ";\n";
+    k << "        unsigned short v[8];\n";
+    k << "        #pragma unroll\n        for (int e = 0; e < 8; ++e) {\n";
+    k << "          const int p = tile_n + grp * 8 + e;\n";
+    k << "          const int img = p / " << OH * OW << ", q = p % " << OH * OW << ";\n";
+    k << "          const int ih = (q / " << OW << ") * " << L.stride[0] << " + rr - " << L.cpad[0] << ";\n";
+    k << "          const int iw = (q % " << OW << ") * " << L.stride[1] << " + ss - " << L.cpad[1] << ";\n";
+    k << "          const bool ok = kg < " << K << " && p < " << NP << " && (unsigned)ih < " << H << "u && (unsigned)iw < "
+      << W << "u;\n";
+    k << "          v[e] = ok ? __ldg(xin + (((size_t)img * " << Cin << " + ci) * " << H << " + ih) * " << W
+      << " + iw) : (unsigned short)0;\n";
+    k << "        }\n";
+    k << "        uint4 pk;\n";
+    k << "        pk.x = v[0] | ((unsigned)v[1] << 16); pk.y = v[2] | ((unsigned)v[3] << 16);\n";
+    k << "        pk.z = v[4] | ((unsigned)v[5] << 16); pk.w = v[6] | ((unsigned)v[7] << 16);\n";
+    // MN-major SW128 canonical: 64-pixel atoms 8 KB apart, K rows 128 B, 16B chunk ^ (row % 8)
+    k << "        st_shared_v4(sb + (grp >> 3) * 8192 + kk * 128 + (((grp & 7) ^ (kk & 7)) << 4), pk);\n";
+    k << "      }\n";
+    k << "      fence_async_smem();\n      __syncwarp();\n";
+    k << "      if (lane == 0) mbar_arrive(full + s);\n";
+    k << "      if (++s == " << S_ << ") { s = 0; ph ^= 1u; }\n    }\n";
+    // weight TMA: warp 4
+    k << "  } else if (warp == 4 && lane == 0) {\n";
+    k << "    int s = 0; unsigned ph = 0;\n";
+    k << "    for (int kb = 0; kb < " << NK << "; ++kb) {\n";
+    k << "      mbar_wait(empty + s, ph ^ 1u);\n";
+    k << "      mbar_expect_tx(full + s, " << A_BYTES << "u);\n";
+    k << "      tma_load_2d(smem + s * " << STAGE << ", &tmA, full + s, kb * 64, tile_m);\n";
+    k << "      if (++s == " << S_ << ") { s = 0; ph ^= 1u; }\n    }\n";
+    // MMA: warp 5
+    k << "  } else if (warp == 5 && lane == 0) {\n";
+    k << "    int s = 0; unsigned ph = 0;\n";
+    k << "    for (int kb = 0; kb < " << NK << "; ++kb) {\n";
+    k << "      mbar_wait(full + s, ph);\n      tc_fence_after();\n";
+    k << "      const unsigned sa = smem_u32(smem + s * " << STAGE << "), sb = sa + " << A_BYTES << ";\n";
+    k << "      #pragma unroll\n      for (int k = 0; k < 4; ++k) {\n";
+    k << "        const unsigned long long ad = umma_desc(sa + k * 32, 16, 1024);\n";
+    k << "        const unsigned long long bd = umma_desc(sb + k * 2048, 8192, 1024);\n";
+    k << "        tc_mma(tmem, ad, bd, " << idesc << "u, (kb | k) != 0);\n      }\n";
+    k << "      tc_commit(empty + s);\n";
+    k << "      if (++s == " << S_ << ") { s = 0; ph ^= 1u; }\n    }\n";
+    k << "    tc_commit(accf);\n  }\n";
+    // epilogue: warps 0-3 (TMEM lane quarters 0-3)
+    k << "  __syncwarp();\n";
+    k << "  if (warp < 4) {\n    mbar_wait(accf, 0);\n    __syncwarp();\n    tc_fence_after();\n";
+    k << "    const int gm = tile_m + warp * 32 + lane;\n    const int tid = 0;\n    (void)tid;\n";
+    k << "    #pragma unroll 1\n    for (int ch = 0; ch < " << BN / 32 << "; ++ch) {\n";
+    k << "      const int nb = tile_n + ch * 32;\n";
+    k << "      float acc[32];\n";
+    k << "      tc_ld32(tmem + ((unsigned)(warp * 32) << 16) + (unsigned)(ch * 32), acc);\n";
+    k << "      if (gm < " << F << " && nb < " << NP << ") {\n";
+    k << ep.body << ep.store;
+    k << "      }\n    }\n  }\n";
+    k << "  tc_fence_before();\n  __syncthreads();\n";
+    k << "  if (warp == 5) tc_dealloc(tmem, " << tcols << ");\n}\n";
+
+    KernelVariant kv;
+    std::string src = k.str();
+    char nm[64];
+    std::snprintf(nm, sizeof nm, "korch_conv_%016llx",
+                  (unsigned long long)fnv1a(std::string(kSm100GemmTemplate) + "\n" + src));
+    kv.name = nm;
+    size_t pos = src.find("KNAME");
+    src.replace(pos, 5, kv.name);
+    kv.source = src;
+    kv.tcgen05 = true;
+    kv.block = 192;
+    kv.grid = Mt;
+    kv.grid_y = Nt;
+    kv.grid_z = 1;
+    kv.smem = smem;
+    kv.tma = {da};
+    std::ostringstream t;
+    t << "conv-igemm BM=128 BN=" << BN << " BK=64 stages=" << S_ << " F=" << F << " P=" << NP << " K=" << K
+      << " (" << R << "x" << S << " s" << L.stride[0] << ")";
+    kv.tag = t.str();
+    kp.variants.push_back(kv);
+  }
+  if (!kp.variants.empty()) {
+    kp.klass = KORCH_CLASS_GEMM;
+    kp.reject.clear();
+  }
+  return kp;
+}
+
 KernelPlan generate_gemm(const Graph& g, const Candidate& c) {
   KernelPlan kp;
   kp.klass = KORCH_CLASS_REJECTED;
@@ -107,10 +287,7 @@ KernelPlan generate_gemm(const Graph& g, const Candidate& c) {
   for (int m : c.members)
     if (g.is_dense_linear(m)) mm = m;
   const Prim& L = g.prims[mm];
-  if (L.kind != Kind::MatMul) {
-    kp.reject = "implicit-GEMM convolution template not available";
-    return kp;
-  }
+  if (L.kind == Kind::Conv2d) return generate_conv_gemm(g, c, mm);
   std::set<int> mem(c.members.begin(), c.members.end());
   View va, vb;
   std::set<int> chain;

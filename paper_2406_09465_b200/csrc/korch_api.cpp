@@ -697,7 +697,21 @@ korch_status korch_profile(korch_graph* G, const int64_t* idx, int64_t n, const 
         if (!m->compiled) continue;
         try {
           int nl = flush ? 1 : launches;
+          int ntr = trials;
           prepare_variant(ctx, s.plan.variants[vi]);
+          {
+            // one probe launch: slow kernels get fewer launches per graph / fewer trials
+            // (the median over >= 3 trials of >= ~100 us of work stays stable)
+            launch_variant(ctx, s.plan, vi, ins, outp, ctx->pstream);
+            CU_CHECK(cu.cuEventRecord(e0, ctx->pstream));
+            launch_variant(ctx, s.plan, vi, ins, outp, ctx->pstream);
+            CU_CHECK(cu.cuEventRecord(e1, ctx->pstream));
+            CU_CHECK(cu.cuEventSynchronize(e1));
+            float ms = 0;
+            CU_CHECK(cu.cuEventElapsedTime(&ms, e0, e1));
+            if (!flush && ms > 0.005f) nl = std::max(1, std::min(nl, (int)(0.1f / ms)));
+            if (ms > 0.2f) ntr = std::min(ntr, 3);
+          }
           CU_CHECK(cu.cuStreamBeginCapture(ctx->pstream, CU_STREAM_CAPTURE_MODE_THREAD_LOCAL));
           try {
             for (int l = 0; l < nl; ++l) launch_variant(ctx, s.plan, vi, ins, outp, ctx->pstream);
@@ -712,9 +726,9 @@ korch_status korch_profile(korch_graph* G, const int64_t* idx, int64_t n, const 
           CUgraphExec ge;
           CU_CHECK(cu.cuGraphInstantiateWithFlags(&ge, graph, 0));
           cu.cuGraphDestroy(graph);
-          for (int w = 0; w < warmup; ++w) CU_CHECK(cu.cuGraphLaunch(ge, ctx->pstream));
+          for (int w = 0; w < (nl < launches ? 1 : warmup); ++w) CU_CHECK(cu.cuGraphLaunch(ge, ctx->pstream));
           std::vector<float> ts;
-          for (int t = 0; t < trials; ++t) {
+          for (int t = 0; t < ntr; ++t) {
             if (flush) CU_CHECK(cu.cuMemsetD8Async(ctx->flush, (unsigned char)t, ctx->flush_bytes, ctx->pstream));
             CU_CHECK(cu.cuEventRecord(e0, ctx->pstream));
             CU_CHECK(cu.cuGraphLaunch(ge, ctx->pstream));

@@ -221,6 +221,34 @@ def test_cnn_primitives(ctx, dtype):
     c.check(sel)
 
 
+def _conv_graph(n, c, h, w, f, k, s, p):
+    b = GraphBuilder("bf16")
+    x = b.input("x", [n, c, h, w])
+    wt = b.input("w", [f, c, k, k], std=(c * k * k) ** -0.5)
+    bias = b.input("b", [f], std=0.1)
+    y = b.op("Conv", x, wt, bias, stride=[s, s], pads=[p, p], groups=1)
+    y = b.op("Relu", y)
+    b.output(y)
+    return b.build()
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("shape", [(1, 16, 20, 24, 32, 3, 1, 1), (1, 32, 17, 19, 48, 3, 2, 1), (2, 64, 14, 14, 160, 1, 1, 0),
+                                   (1, 128, 28, 28, 128, 3, 1, 1), (1, 32, 30, 30, 64, 5, 2, 2)])
+def test_conv_igemm_every_variant(ctx, shape):
+    """tcgen05 implicit-GEMM convolution (KB6): every launch variant of every conv
+    candidate (conv alone, + bias, + bias + ReLU), strides, zero padding, filter / pixel
+    tails, batch > 1."""
+    c = Case(ctx, _conv_graph(*shape))
+    convs = [x for x in c.cands if x["klass"] == "gemm"]
+    assert convs, "conv candidates must be accepted by the implicit-GEMM template"
+    for x in convs:
+        nv, _, _ = c.kg.variant_info(x["index"])
+        for v in range(nv):
+            c.kg.set_variant(x["index"], v)
+            c.check(c.completion([x["index"]]))
+
+
 @pytest.mark.gpu
 def test_c2_every_gemm_candidate(ctx):
     """Every tcgen05 GEMM candidate of the ViT attention layer (fused views + epilogues)."""
