@@ -226,6 +226,41 @@ def run_models(K, names, oracle_check=True):
     return res
 
 
+def scaled_variant(K, pk, batch=64, steps=10):
+    """C2 at batch 64 (M = 8192 tokens; SURVEY.md §8(d) C2 scale list): tune, select,
+    time; the dominant kernel re-timed cold against the tensor (or HBM) roofline."""
+    import torch
+    from korch_workloads import make_inputs
+    graph, cfg = config_graph("c2", batch)
+    ctx = K.Context(torch.cuda.current_device())
+    kg = K.KorchGraph(ctx, graph)
+    cands = kg.enumerate()
+    costs = kg.profile()
+    obj, sel = kg.select(costs)
+    ins = make_inputs(graph, seed=0)
+    dev = K.torch_inputs(graph, {k: v[1] for k, v in ins.items()})
+    ms, _ = time_plan(kg, sel, dev, steps=steps)
+    order = kg.plan()
+    dom = max(order, key=lambda i: costs[i])
+    cold = kg.profile([dom], flush_l2=True, trials=7)[0]
+    dc = cands[dom]
+    flops = sum(cands[i]["flops"] for i in order)
+    res = {"workload": f"C2 ViT-B MHSA layer, batch {batch} x seq 128 (M = {batch * 128}), bf16",
+           "ms": ms, "kernels": len(order), "tflops_plan": flops / (ms * 1e-3) / 1e12,
+           "dominant": {"candidate": dom, "class": dc["klass"], "members": len(dc["members"]),
+                        "ns_cold_l2": cold, "variant": kg.variant_info(dom)[2], "name": dc["signature"]}}
+    if dc["flops"] > 0:
+        t = dc["flops"] / (cold * 1e-9) / 1e12
+        res["dominant"].update({"bound": "tensor", "achieved_tflops": t, "peak_tflops": pk["bf16_tflops"],
+                                "frac": t / pk["bf16_tflops"]})
+    else:
+        gbs = dc["bytes"] / cold
+        res["dominant"].update({"bound": "hbm", "achieved_gbs": gbs, "peak_gbs": pk["hbm_gbs"],
+                                "frac": gbs / pk["hbm_gbs"]})
+    ctx.close()
+    return res
+
+
 def bandwidth_variant(K, pk, steps=10):
     """C1 at x[2^20,128] fp32 (SURVEY.md §8(d) C1 bandwidth variant): enumerate, profile
     (cold, inputs > L2), BLP-select, execute; achieved GB/s of the plan and of its
@@ -311,6 +346,7 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-bw-variant", action="store_true", help="skip the C1 x[2^20,128] bandwidth measurement")
     ap.add_argument("--models", default="", help="comma list of whole models to tune and time (candy,segformer)")
+    ap.add_argument("--no-scaled", action="store_true", help="skip the C2 batch-64 measurement")
     ap.add_argument("--cpu-budget", type=float, default=15.0)
     ap.add_argument("--save-selection", default=None, help="write the chosen plan (for tools/replay.py)")
     args = ap.parse_args()
@@ -480,6 +516,12 @@ def main():
     models = None
     if rank == 0 and world == 1 and args.models:
         models = run_models(K, [m for m in args.models.split(",") if m])
+    scaled = None
+    if rank == 0 and world == 1 and not args.no_scaled and args.config == "c2":
+        try:
+            scaled = scaled_variant(K, pk)
+        except Exception as e:
+            scaled = {"error": str(e)[:300]}
     bw = None
     if rank == 0 and world == 1 and not args.no_bw_variant:
         try:
@@ -508,6 +550,7 @@ def main():
             "models": models,
             "roofline": roof,
             "bandwidth_variant": bw,
+            "scaled_variant": scaled,
             "cpu_baseline": cpu,
             "clocks": clk.summary(),
             "tuning": tuning,
