@@ -234,7 +234,7 @@ def scaled_variant(K, pk, batch=64, steps=10):
     graph, cfg = config_graph("c2", batch)
     ctx = K.Context(torch.cuda.current_device())
     kg = K.KorchGraph(ctx, graph)
-    cands = kg.enumerate()
+    cands = kg.enumerate(attention_pairs=True)
     costs = kg.profile()
     obj, sel = kg.select(costs)
     ins = make_inputs(graph, seed=0)
@@ -347,6 +347,8 @@ def main():
     ap.add_argument("--no-bw-variant", action="store_true", help="skip the C1 x[2^20,128] bandwidth measurement")
     ap.add_argument("--models", default="", help="comma list of whole models to tune and time (candy,segformer)")
     ap.add_argument("--no-scaled", action="store_true", help="skip the C2 batch-64 measurement")
+    ap.add_argument("--no-attention-pairs", action="store_true",
+                    help="paper-faithful P:626 prune only (no fused two-GEMM attention candidates)")
     ap.add_argument("--cpu-budget", type=float, default=15.0)
     ap.add_argument("--save-selection", default=None, help="write the chosen plan (for tools/replay.py)")
     args = ap.parse_args()
@@ -374,7 +376,8 @@ def main():
     ctx = K.Context(local)
     kg = K.KorchGraph(ctx, graph)
     t0 = time.perf_counter()
-    cands = kg.enumerate()
+    # NEXT item N2: two-GEMM attention candidates join the search
+    cands = kg.enumerate(attention_pairs=not args.no_attention_pairs)
     t_enum = time.perf_counter() - t0
     t0 = time.perf_counter()
     kg.compile()
@@ -391,6 +394,7 @@ def main():
     order = kg.plan()
     if args.save_selection:
         json.dump({"config": args.config, "batch": 1, "selection": sel,
+                   "attention_pairs": not args.no_attention_pairs,
                    "variants": {str(i): kg.variant_info(i)[1] for i in order},
                    "tags": {str(i): kg.variant_info(i)[2] for i in order},
                    "kernels": {str(i): cands[i]["signature"] for i in order},

@@ -65,6 +65,8 @@ typedef struct {
   int64_t max_states;         /* KORCH_E_STATE_EXPLOSION above this; default 1,000,000       */
   int32_t partition_max;      /* > 0: partition (reading A17) into parts of about this
                                  many primitives; 0: only graphs > 256 primitives, parts of 64 */
+  int32_t attention_pairs;    /* 1: keep candidates with two MatMuls where the first feeds the
+                                 second's A operand (fused attention; NEXT item N2) */
 } korch_enum_opts;
 
 /* One candidate kernel (P', o): a convex set with a unique sink o (reading A4). */

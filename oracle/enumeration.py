@@ -124,10 +124,12 @@ def sinks(g: PGraph, s):
     return [v for v in s if not any(w in s for w in g.succs[v])]
 
 
-def candidates(g: PGraph, convex_sets, max_prims=16, prune_linear=True):
+def candidates(g: PGraph, convex_sets, max_prims=16, prune_linear=True, attention_pairs=False):
     """Unique-sink candidates (A4) after the P:626 pruning, in canonical order.
 
     Canonical order: sort by (output id, popcount, member-id tuple).
+    attention_pairs (NEXT item N2): keep a candidate with exactly two dense
+    linears L1, L2 when L1 feeds L2's first operand (the A side) and not its second.
     Returns a list of (members: tuple sorted, output: int).
     """
     pg = g.pg
@@ -140,6 +142,16 @@ def candidates(g: PGraph, convex_sets, max_prims=16, prune_linear=True):
                        for r in nd["inputs"]]
                 if is_dense_linear(nd, ins):
                     dense.add(nd["id"])
+    reach = g.reach() if attention_pairs else None
+
+    def attention_ok(pair):
+        a, b = sorted(pair, key=lambda v: g.topo_index[v])
+        ins = pg["nodes"][b]["inputs"]
+        if pg["nodes"][a]["kind"] != "matmul" or pg["nodes"][b]["kind"] != "matmul":
+            return False
+        feeds = lambda r: r[0] == "node" and (r[1] == a or r[1] in reach[a])
+        return feeds(ins[0]) and not feeds(ins[1])
+
     out = []
     for s in convex_sets:
         sk = sinks(g, s)
@@ -147,8 +159,10 @@ def candidates(g: PGraph, convex_sets, max_prims=16, prune_linear=True):
             continue
         if len(s) > max_prims:
             continue
-        if prune_linear and len(dense & s) >= 2:
-            continue
+        if prune_linear:
+            d = dense & s
+            if len(d) > 2 or (len(d) == 2 and not (attention_pairs and attention_ok(d))):
+                continue
         out.append((tuple(sorted(s)), sk[0]))
     out.sort(key=lambda c: (c[1], len(c[0]), c[0]))
     return out

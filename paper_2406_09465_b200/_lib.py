@@ -43,7 +43,7 @@ class KorchError(RuntimeError):
 
 class EnumOpts(C.Structure):
     _fields_ = [("max_prims", C.c_int32), ("keep_multi_linear", C.c_int32), ("max_states", C.c_int64),
-                ("partition_max", C.c_int32)]
+                ("partition_max", C.c_int32), ("attention_pairs", C.c_int32)]
 
 
 class CandDesc(C.Structure):

@@ -85,8 +85,8 @@ class KorchGraph:
 
     # ---------------------------------------------------------------- candidates
     def enumerate(self, max_prims: int = 16, keep_multi_linear: bool = False, max_states: int = 1_000_000,
-                  partition_max: int = 0):
-        o = _lib.EnumOpts(max_prims, int(keep_multi_linear), max_states, partition_max)
+                  partition_max: int = 0, attention_pairs: bool = False):
+        o = _lib.EnumOpts(max_prims, int(keep_multi_linear), max_states, partition_max, int(attention_pairs))
         nc, ns = C.c_int64(), C.c_int64()
         check(LIB.korch_enumerate(self.h, C.byref(o), C.byref(nc), C.byref(ns)))
         self.n_states = ns.value

@@ -58,8 +58,11 @@ struct GemmEpilogue {
   int64_t bytes = 0;                  // epilogue reads + output write
   std::vector<std::string> batch_vars;
 };
+// target >= 0: compute that intermediate node instead of the candidate's output; then
+// `store` holds the name of the float[cw] array with its values (no global store).
 bool make_gemm_epilogue(const Graph& g, const Candidate& c, int mm, int cw, const std::vector<Ref>& pre_ext,
-                        GemmEpilogue* out, std::string* err);
+                        GemmEpilogue* out, std::string* err, int target = -1);
+KernelPlan generate_attention(const Graph& g, const Candidate& c);   // gemm_gen.cpp (N2)
 KernelPlan generate_gemm(const Graph& g, const Candidate& c);   // gemm_gen.cpp
 std::string kernel_prelude();
 std::string fmt_float(double v);

@@ -148,6 +148,37 @@ std::vector<Candidate> enumerate_candidates(const Graph& g, const EnumOpts& o, i
       for (int w : g.succs[part[i]])
         if (loc[w] >= 0) succ_bits[i].set(loc[w]);
     }
+    // descendants within the part (for the attention-pair rule, N2)
+    std::vector<Bits> desc(m);
+    if (o.attention_pairs) {
+      std::vector<int> order_local;
+      for (int v : g.topo)
+        if (loc[v] >= 0) order_local.push_back(loc[v]);
+      for (auto it = order_local.rbegin(); it != order_local.rend(); ++it) {
+        int v = *it;
+        for (int w : g.succs[part[v]])
+          if (loc[w] >= 0) {
+            desc[v].set(loc[w]);
+            for (int i = 0; i < kMaxPrims / 64; ++i) desc[v].w[i] |= desc[loc[w]].w[i];
+          }
+      }
+    }
+    auto attention_ok = [&](const std::vector<int>& mem_local) {
+      std::vector<int> lin;
+      for (int v : mem_local)
+        if (dense[part[v]]) lin.push_back(v);
+      if (lin.size() != 2) return false;
+      int a = lin[0], b = lin[1];
+      if (g.topo_index[part[a]] > g.topo_index[part[b]]) std::swap(a, b);
+      const Prim& pa = g.prims[part[a]];
+      const Prim& pb = g.prims[part[b]];
+      if (pa.kind != Kind::MatMul || pb.kind != Kind::MatMul) return false;
+      auto feeds = [&](const Ref& r) {
+        if (r.is_input || loc[r.id] < 0) return false;
+        return loc[r.id] == a || desc[a].test(loc[r.id]);
+      };
+      return feeds(pb.in[0]) && !feeds(pb.in[1]);
+    };
     Bits empty;
     d.B.insert(empty);  // reading A1: seed B with the empty state
     d.order.push_back(empty);
@@ -172,7 +203,9 @@ std::vector<Candidate> enumerate_candidates(const Graph& g, const EnumOpts& o, i
           nd += dense[part[v]];
         }
         if (nsink != 1) continue;                         // single output (A4)
-        if (!o.keep_multi_linear && nd >= 2) continue;    // P:626 (A18)
+        if (!o.keep_multi_linear && nd >= 2 &&            // P:626 (A18), relaxed for N2
+            !(nd == 2 && o.attention_pairs && attention_ok(mem_local)))
+          continue;
         Candidate c;
         for (int v : mem_local) c.members.push_back(part[v]);
         std::sort(c.members.begin(), c.members.end());

@@ -71,6 +71,7 @@ struct EnumOpts {
   bool keep_multi_linear = false;
   int64_t max_states = 1000000;
   int partition_max = 0;          // > 0: partition into parts of about this many primitives
+  bool attention_pairs = false;   // N2: keep MatMul pairs where the first feeds the second's A
 };
 
 // Reading A17: parts of the topological order separated at articulation tensors.

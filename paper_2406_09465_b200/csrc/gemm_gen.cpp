@@ -611,4 +611,212 @@ KernelPlan generate_gemm(const Graph& g, const Candidate& c) {
   return kp;
 }
 
+
+// N2: fused two-GEMM attention candidate.  S = A1 * B1 lands
+// in TMEM; the softmax-like chain from S to P (elementwise ops + in-tile row reductions,
+// one thread per row) runs in registers and writes P as bf16 straight into shared memory
+// in the canonical K-major 128B-swizzled layout; O = P * V is issued on the tensor core
+// from that smem; O's fused epilogue (views folded into the store) writes the output.
+// Q, K^T and V reach shared memory by TMA through their strided views.  P never
+// touches HBM.  Single pass: the whole row (N1 <= 256) is in one tile.
+KernelPlan generate_attention(const Graph& g, const Candidate& c) {
+  KernelPlan kp;
+  kp.klass = KORCH_CLASS_REJECTED;
+  std::vector<int> lin;
+  for (int m : c.members)
+    if (g.is_dense_linear(m)) lin.push_back(m);
+  if (lin.size() != 2) { kp.reject = "expected two linear primitives"; return kp; }
+  if (g.topo_index[lin[0]] > g.topo_index[lin[1]]) std::swap(lin[0], lin[1]);
+  const Prim& L1 = g.prims[lin[0]];
+  const Prim& L2 = g.prims[lin[1]];
+  if (L1.kind != Kind::MatMul || L2.kind != Kind::MatMul) { kp.reject = "attention needs two MatMuls"; return kp; }
+  std::set<int> mem(c.members.begin(), c.members.end());
+  if (L2.in[0].is_input || !mem.count(L2.in[0].id)) { kp.reject = "P must be computed in the kernel"; return kp; }
+  const int pnode = L2.in[0].id;
+  View vq, vk, vv;
+  std::set<int> chain;
+  std::string err;
+  if (!operand_view(g, mem, L1, 0, &vq, &chain, &err) || !operand_view(g, mem, L1, 1, &vk, &chain, &err) ||
+      !operand_view(g, mem, L2, 1, &vv, &chain, &err)) {
+    kp.reject = err;
+    return kp;
+  }
+  for (auto* v : {&vq, &vk, &vv})
+    if (g.dtype_of(v->src) != DType::BF16 || (v->off * 2) % 16) { kp.reject = "attention operands must be aligned bf16"; return kp; }
+  const Shape& SS = L1.shape;  // [batch..., M, N1]
+  const Shape& OS = L2.shape;  // [batch..., M, N2]
+  int nb = (int)SS.size() - 2;
+  int64_t M = SS[nb], N1 = SS[nb + 1], K1 = vq.shape.back(), N2 = OS.back();
+  if ((int)OS.size() != (int)SS.size() || (int)vq.shape.size() != nb + 2 || (int)vk.shape.size() != nb + 2 ||
+      (int)vv.shape.size() != nb + 2) {
+    kp.reject = "attention batch dims";
+    return kp;
+  }
+  if (N1 % 64 || N1 > 256 || K1 > 128 || N2 % 16 || N2 > 256 || N1 + N2 > 512) {
+    kp.reject = "attention tile limits (N1 % 64, N1 <= 256, K1 <= 128, N2 <= 256)";
+    return kp;
+  }
+  bool q_k = vq.coef[nb + 1] == 1, k_k = vk.coef[nb] == 1, v_n = vv.coef[nb + 1] == 1, v_k = vv.coef[nb] == 1;
+  if (!q_k || !k_k || !(v_n || v_k)) { kp.reject = "attention operand majorness"; return kp; }
+  // pass 1: P from the S accumulator (full row, in-tile reductions)
+  std::vector<Ref> pre{vq.src, vk.src, vv.src};
+  GemmEpilogue ep1, ep2;
+  if (!make_gemm_epilogue(g, c, lin[0], (int)N1, pre, &ep1, &err, pnode)) { kp.reject = "P: " + err; return kp; }
+  if (!make_gemm_epilogue(g, c, lin[1], 32, ep1.ext, &ep2, &err)) { kp.reject = "O: " + err; return kp; }
+  kp.ext = ep2.ext;
+  auto slot_of = [&](const Ref& r) {
+    for (size_t i = 0; i < kp.ext.size(); ++i)
+      if (kp.ext[i].is_input == r.is_input && kp.ext[i].id == r.id) return (int)i;
+    return -1;
+  };
+  int sq = slot_of(vq.src), sk = slot_of(vk.src), sv = slot_of(vv.src);
+  auto desc = [&](const View& v, int slot, int64_t inner, int64_t outer, int64_t outer_coef, uint32_t bi, uint32_t bo,
+                  std::vector<int>* baxes, TmaDesc* d) {
+    d->tensor = slot; d->dtype = 1; d->swizzle = 3; d->elem_off = v.off; d->rank = 0;
+    auto push = [&](int64_t dim, int64_t st, uint32_t box) {
+      d->dims[d->rank] = dim; d->strides[d->rank] = st * 2; d->box[d->rank] = box; d->rank++;
+    };
+    push(inner, 1, bi);
+    push(outer, outer_coef ? outer_coef : inner, bo);
+    for (int b = 0; b < nb; ++b)
+      if (v.coef[b] != 0 && v.shape[b] > 1) {
+        if (d->rank >= 5) return false;
+        push(v.shape[b], v.coef[b], 1);
+        baxes->push_back(b);
+      }
+    for (int i = 1; i < d->rank; ++i)
+      if (d->strides[i] % 16) return false;
+    return true;
+  };
+  TmaDesc dq, dk, dv;
+  std::vector<int> bq, bk, bv;
+  bool ok = desc(vq, sq, K1, M, vq.coef[nb], 64, 128, &bq, &dq) && desc(vk, sk, K1, N1, vk.coef[nb + 1], 64, (uint32_t)N1, &bk, &dk);
+  ok = ok && (v_n ? desc(vv, sv, N2, N1, vv.coef[nb], 64, (uint32_t)N1, &bv, &dv)
+                  : desc(vv, sv, N1, N2, vv.coef[nb + 1], 64, (uint32_t)N2, &bv, &dv));
+  if (!ok) { kp.reject = "attention operand strides not expressible as TMA maps"; return kp; }
+  int64_t batch = 1;
+  for (int b = 0; b < nb; ++b) batch *= SS[b];
+  const int64_t KB1 = (K1 + 63) / 64;
+  const int Q_BYTES = (int)(KB1 * 16384), K_BYTES = (int)(KB1 * N1 * 128);
+  const int V_BYTES = (int)(v_n ? ((N2 + 63) / 64) * N1 * 128 : (N1 / 64) * N2 * 128);
+  const int P_BYTES = (int)((N1 / 64) * 16384);
+  const int offK = Q_BYTES, offV = offK + K_BYTES, offP = offV + V_BYTES, offB = offP + P_BYTES;
+  const int smem = offB + 64 + 1024;
+  const int tcols = N1 + N2 <= 256 ? 256 : 512;
+  const uint32_t id1 = (1u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(N1 >> 3) << 17) | ((uint32_t)(128 >> 4) << 24);
+  const uint32_t id2 = (1u << 4) | (1u << 7) | (1u << 10) | ((v_n ? 1u : 0u) << 16) | ((uint32_t)(N2 >> 3) << 17) |
+                       ((uint32_t)(128 >> 4) << 24);
+  kp.flops = 2.0 * batch * M * (N1 * K1 + N2 * N1);
+  kp.bytes = ep2.bytes + ep1.bytes - 0 + 2 * (numel(vq.shape) + numel(vk.shape) + numel(vv.shape));
+  auto coords = [&](const std::string& inner, const std::string& outer, const std::vector<int>& baxes) {
+    std::string s = inner + ", " + outer;
+    for (int b : baxes) s += ", " + std::string("bz") + std::to_string(b);
+    return s;
+  };
+  auto load = [&](int rank) { return "tma_load_" + std::to_string(rank) + "d"; };
+  std::ostringstream k;
+  k << "extern \"C\" __global__ void __launch_bounds__(192, 1) KNAME(";
+  for (size_t i = 0; i < kp.ext.size(); ++i)
+    k << "const " << (g.dtype_of(kp.ext[i]) == DType::F32 ? "float" : "bf16_t") << "* __restrict__ p" << i << ", ";
+  k << (g.prims[c.output].dtype == DType::F32 ? "float" : "bf16_t") << "* __restrict__ out, "
+    << "const __grid_constant__ TmaMap tmQ, const __grid_constant__ TmaMap tmK, const __grid_constant__ TmaMap tmV) {\n";
+  k << "  typedef int idx_t;\n";
+  k << "  extern __shared__ __align__(1024) unsigned char smem_raw[];\n";
+  k << "  unsigned char* smem = (unsigned char*)(((unsigned long long)smem_raw + 1023ull) & ~1023ull);\n";
+  k << "  unsigned long long* bars = (unsigned long long*)(smem + " << offB << ");\n";
+  k << "  unsigned long long *ldf = bars, *sfull = bars + 1, *pfull = bars + 2, *ofull = bars + 3;\n";
+  k << "  unsigned* tslot = (unsigned*)(bars + 4);\n";
+  k << "  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;\n";
+  k << "  const int tile_m = blockIdx.x * 128;\n";
+  k << "  int bzl = blockIdx.z;\n";
+  for (int b = nb - 1; b >= 0; --b) k << "  const int bz" << b << " = bzl % " << SS[b] << "; bzl /= " << SS[b] << ";\n";
+  k << "  (void)bzl;\n";
+  k << "  if (threadIdx.x == 0) {\n    mbar_init(ldf, 1); mbar_init(sfull, 1); mbar_init(pfull, 4); mbar_init(ofull, 1);\n"
+    << "    mbar_fence_init();\n    tma_prefetch(&tmQ); tma_prefetch(&tmK); tma_prefetch(&tmV);\n  }\n";
+  k << "  if (warp == 5) tc_alloc(tslot, " << tcols << ");\n";
+  k << "  tc_fence_before();\n  __syncthreads();\n  tc_fence_after();\n";
+  k << "  const unsigned tmem = *tslot;\n";
+  k << "  pdl_trigger();\n  pdl_wait();\n";
+  // TMA: warp 4
+  k << "  if (warp == 4 && lane == 0) {\n";
+  k << "    mbar_expect_tx(ldf, " << Q_BYTES + K_BYTES + V_BYTES << "u);\n";
+  for (int64_t kb = 0; kb < KB1; ++kb) {
+    k << "    " << load(dq.rank) << "(smem + " << kb * 16384 << ", &tmQ, ldf, " << coords(std::to_string(kb * 64), "tile_m", bq) << ");\n";
+    k << "    " << load(dk.rank) << "(smem + " << offK + kb * N1 * 128 << ", &tmK, ldf, " << coords(std::to_string(kb * 64), "0", bk) << ");\n";
+  }
+  if (v_n) {
+    for (int64_t cc = 0; cc < (N2 + 63) / 64; ++cc)
+      k << "    " << load(dv.rank) << "(smem + " << offV + cc * N1 * 128 << ", &tmV, ldf, " << coords(std::to_string(cc * 64), "0", bv) << ");\n";
+  } else {
+    for (int64_t cc = 0; cc < N1 / 64; ++cc)
+      k << "    " << load(dv.rank) << "(smem + " << offV + cc * N2 * 128 << ", &tmV, ldf, " << coords(std::to_string(cc * 64), "0", bv) << ");\n";
+  }
+  // MMA: warp 5
+  k << "  } else if (warp == 5 && lane == 0) {\n";
+  k << "    mbar_wait(ldf, 0);\n    tc_fence_after();\n";
+  k << "    const unsigned sq = smem_u32(smem), sk = sq + " << offK << ", sv = sq + " << offV << ", sp = sq + " << offP << ";\n";
+  k << "    #pragma unroll\n    for (int kb = 0; kb < " << KB1 << "; ++kb)\n";
+  k << "      #pragma unroll\n      for (int k = 0; k < 4; ++k)\n";
+  k << "        tc_mma(tmem, umma_desc(sq + kb * 16384 + k * 32, 16, 1024), umma_desc(sk + kb * " << N1 * 128
+    << " + k * 32, 16, 1024), " << id1 << "u, (kb | k) != 0);\n";
+  k << "    tc_commit(sfull);\n";
+  k << "    mbar_wait(pfull, 0);\n    tc_fence_after();\n";
+  k << "    #pragma unroll\n    for (int k0 = 0; k0 < " << N1 << "; k0 += 16) {\n";
+  k << "      const unsigned long long ad = umma_desc(sp + (k0 >> 6) * 16384 + (k0 & 63) * 2, 16, 1024);\n";
+  if (v_n)
+    k << "      const unsigned long long bd = umma_desc(sv + k0 * 128, " << N1 * 128 << ", 1024);\n";
+  else
+    k << "      const unsigned long long bd = umma_desc(sv + (k0 >> 6) * " << N2 * 128 << " + (k0 & 63) * 2, 16, 1024);\n";
+  k << "      tc_mma(tmem + " << N1 << ", ad, bd, " << id2 << "u, k0 != 0);\n    }\n";
+  k << "    tc_commit(ofull);\n  }\n";
+  k << "  __syncwarp();\n";
+  // epilogue warps 0-3: P into smem, then O to HBM
+  k << "  if (warp < 4) {\n";
+  k << "    const int gm = tile_m + warp * 32 + lane;\n    const int tid = 0;\n    (void)tid;\n";
+  k << "    mbar_wait(sfull, 0);\n    __syncwarp();\n    tc_fence_after();\n";
+  k << "    {\n      const int nb = 0;\n      float acc[" << N1 << "];\n";
+  k << "      #pragma unroll\n      for (int q = 0; q < " << N1 / 32 << "; ++q)\n"
+    << "        tc_ld32(tmem + ((unsigned)(warp * 32) << 16) + (unsigned)(q * 32), acc + q * 32);\n";
+  k << ep1.body;
+  k << "      const unsigned sp = smem_u32(smem + " << offP << ");\n";
+  k << "      const int r = warp * 32 + lane;\n";
+  k << "      #pragma unroll\n      for (int q = 0; q < " << N1 / 8 << "; ++q) {\n";
+  k << "        uint4 pk = make_uint4(pack2(" << ep1.store << "[q * 8], " << ep1.store << "[q * 8 + 1]), pack2(" << ep1.store
+    << "[q * 8 + 2], " << ep1.store << "[q * 8 + 3]), pack2(" << ep1.store << "[q * 8 + 4], " << ep1.store << "[q * 8 + 5]), pack2("
+    << ep1.store << "[q * 8 + 6], " << ep1.store << "[q * 8 + 7]));\n";
+  k << "        st_shared_v4(sp + (q >> 3) * 16384 + r * 128 + (((q & 7) ^ (r & 7)) << 4), pk);\n      }\n";
+  k << "    }\n";
+  k << "    fence_async_smem();\n    tc_fence_before();\n    __syncwarp();\n    if (lane == 0) mbar_arrive(pfull);\n";
+  k << "    mbar_wait(ofull, 0);\n    __syncwarp();\n    tc_fence_after();\n";
+  k << "    #pragma unroll 1\n    for (int ch = 0; ch < " << (N2 + 31) / 32 << "; ++ch) {\n";
+  k << "      const int nb = ch * 32;\n      float acc[32];\n";
+  k << "      tc_ld32(tmem + ((unsigned)(warp * 32) << 16) + (unsigned)(" << N1 << " + ch * 32), acc);\n";
+  k << "      if (gm < " << M << " && nb < " << N2 << ") {\n";
+  k << ep2.body << ep2.store;
+  k << "      }\n    }\n  }\n";
+  k << "  tc_fence_before();\n  __syncthreads();\n";
+  k << "  if (warp == 5) tc_dealloc(tmem, " << tcols << ");\n}\n";
+  KernelVariant kv;
+  std::string src = k.str();
+  char nm[64];
+  std::snprintf(nm, sizeof nm, "korch_attn_%016llx", (unsigned long long)fnv1a(std::string(kSm100GemmTemplate) + "\n" + src));
+  kv.name = nm;
+  src.replace(src.find("KNAME"), 5, kv.name);
+  kv.source = src;
+  kv.tcgen05 = true;
+  kv.block = 192;
+  kv.grid = (M + 127) / 128;
+  kv.grid_y = 1;
+  kv.grid_z = batch;
+  kv.smem = smem;
+  kv.tma = {dq, dk, dv};
+  std::ostringstream t;
+  t << "attention BM=128 N1=" << N1 << " K1=" << K1 << " N2=" << N2 << " V=" << (v_n ? "N" : "K") << "-major batch=" << batch;
+  kv.tag = t.str();
+  kp.variants.push_back(kv);
+  kp.klass = KORCH_CLASS_GEMM;
+  kp.reject.clear();
+  return kp;
+}
+
 }  // namespace korch

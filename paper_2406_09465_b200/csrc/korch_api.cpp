@@ -536,6 +536,7 @@ korch_status korch_enumerate(korch_graph* G, const korch_enum_opts* o, int64_t* 
       eo.keep_multi_linear = o->keep_multi_linear != 0;
       if (o->max_states > 0) eo.max_states = o->max_states;
       if (o->partition_max > 0) eo.partition_max = o->partition_max;
+      eo.attention_pairs = o->attention_pairs != 0;
     }
     std::lock_guard<std::mutex> lk(G->mu);
     G->cands = enumerate_candidates(G->g, eo, &G->n_states);

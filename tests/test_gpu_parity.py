@@ -250,6 +250,27 @@ def test_conv_igemm_every_variant(ctx, shape):
 
 
 @pytest.mark.gpu
+@pytest.mark.parametrize("kw", [dict(), dict(batch=2, seq=64, hidden=256, heads=4), dict(seq=200, hidden=192, heads=3)])
+def test_fused_attention_candidates(ctx, kw):
+    """NEXT item N2: two-GEMM attention candidates (QK^T -> in-tile softmax ->
+    P V, P kept in shared memory) against the oracle, and a BLP plan that may use them."""
+    from paper_2406_09465_b200 import KorchGraph
+    g = c2_vit_attention(**kw)
+    c = Case(ctx, g)
+    c.cands = c.kg.enumerate(attention_pairs=True)
+    c.ref = candidates(c.G, convex_sets_from_states(execution_states(c.G)), 16, attention_pairs=True)
+    assert [(tuple(x["members"]), x["output"]) for x in c.cands] == [(tuple(m), o) for m, o in c.ref]
+    att = [x["index"] for x in c.cands if x["n_dense_linear"] == 2 and x["klass"] == "gemm"]
+    if kw.get("seq", 128) % 64 == 0:
+        assert att
+    for i in att:
+        c.check(c.completion([i]))
+    costs = c.kg.profile()
+    obj, sel = c.kg.select(costs)
+    c.check(sel)
+
+
+@pytest.mark.gpu
 def test_c2_every_gemm_candidate(ctx):
     """Every tcgen05 GEMM candidate of the ViT attention layer (fused views + epilogues)."""
     c = Case(ctx, c2_vit_attention())

@@ -18,7 +18,7 @@ def main():
     from bench import config_graph
     graph, _ = config_graph(sel["config"], sel.get("batch", 1))
     kg = K.KorchGraph(K.Context(-1), graph)
-    cands = kg.enumerate()
+    cands = kg.enumerate(attention_pairs=sel.get("attention_pairs", False))
     costs = sel["all_costs_ns"]
     var = sel["all_variants"]
     kinds = {n["id"]: n["kind"] for n in kg.prim["nodes"]}

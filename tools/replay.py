@@ -32,7 +32,7 @@ def main():
     graph, _ = config_graph(sel["config"], sel.get("batch", 1))
     ctx = K.Context(0)
     kg = K.KorchGraph(ctx, graph)
-    kg.enumerate()
+    kg.enumerate(attention_pairs=sel.get("attention_pairs", False))
     kg.set_orchestration(sel["selection"], variants=sel.get("variants"))
     ins = make_inputs(graph, seed=0)
     dev = K.torch_inputs(graph, {k: v[1] for k, v in ins.items()})
