@@ -182,7 +182,11 @@ def run_models(K, names, oracle_check=True):
         graph = MODELS[name]()
         ctx = K.Context(torch.cuda.current_device())
         kg = K.KorchGraph(ctx, graph)
-        cands = kg.enumerate(partition_max=64, max_prims=MODEL_MAX_PRIMS)
+        # the operator-aligned baseline needs every operator's fragment as a candidate
+        frag = {}
+        for n in kg.prim["nodes"]:
+            frag[n["op"]] = frag.get(n["op"], 0) + 1
+        cands = kg.enumerate(partition_max=64, max_prims=max(MODEL_MAX_PRIMS, max(frag.values())))
         t_enum = time.perf_counter() - t0
         t1 = time.perf_counter()
         kg.compile()
@@ -362,10 +366,17 @@ def main():
 
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
-    local = int(os.environ.get("LOCAL_RANK", "0"))
+    # one process per GPU; KORCH_DIST_BACKEND=gloo + more ranks than GPUs is a test mode
+    # that exercises the multi-rank logic on one device
+    backend = os.environ.get("KORCH_DIST_BACKEND", "nccl")
+    local = int(os.environ.get("LOCAL_RANK", "0")) % max(1, torch.cuda.device_count())
     torch.cuda.set_device(local)
+    coll_dev = "cuda" if backend == "nccl" else None
     if world > 1:
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        else:
+            dist.init_process_group(backend)
 
     import paper_2406_09465_b200 as K
     from korch_workloads import make_inputs
@@ -383,10 +394,24 @@ def main():
     kg.compile()
     t_compile = time.perf_counter() - t0
     t0 = time.perf_counter()
-    costs = kg.profile()
+    from paper_2406_09465_b200.dist import broadcast_selection, merge_costs, my_share
+    if world > 1:
+        # profiling sharded across the GPUs (G1: MIN all-reduce of costs + variants)
+        mine = my_share(len(cands), rank, world)
+        local = kg.profile(mine)
+        costs, variants = merge_costs(mine, local, [kg.variant_info(i)[1] for i in mine], len(cands),
+                                      device=coll_dev)
+        for i, v in enumerate(variants):
+            if v >= 0:
+                kg.set_variant(i, v)
+    else:
+        costs = kg.profile()
     t_prof = time.perf_counter() - t0
     t0 = time.perf_counter()
     obj, sel = kg.select(costs)
+    if world > 1:
+        sel = broadcast_selection(sel, src=0, device=coll_dev)   # G2: rank 0's selection
+        obj = sum(costs[i] for i in sel)
     t_sel = time.perf_counter() - t0
     base = kg.operator_aligned()
     base_obj = sum(costs[i] for i in base) if all(costs[i] < K.INF for i in base) else None
@@ -510,7 +535,15 @@ def main():
 
     # gather max over ranks (G4): a step takes as long as its slowest rank
     from paper_2406_09465_b200.dist import max_over_ranks
-    ms_max, e2e_max = max_over_ranks([ms, e2e_ms], device="cuda")
+    ms_max, e2e_max = max_over_ranks([ms, e2e_ms], device=coll_dev)
+    # G3: gather every replica's output (outside the timed region); identical inputs and an
+    # identical orchestration must give bitwise-identical outputs on every GPU
+    replicas_agree = None
+    if world > 1:
+        o0 = outs[0].contiguous() if coll_dev else outs[0].float().cpu()
+        gathered = [torch.empty_like(o0) for _ in range(world)]
+        dist.all_gather(gathered, o0)
+        replicas_agree = all(torch.equal(gathered[0], x) for x in gathered[1:])
 
     # the operator-aligned orchestration measured end to end (BASELINE target)
     base_ms = None
@@ -543,6 +576,9 @@ def main():
             "config": dict(cfg, batch_per_gpu=1, global_batch=world, l2="flushed between steps (512 MiB write)",
                            parallelism=f"replicas x{world}"),
             "throughput": {"value": world * 1e3 / ms_max, "unit": "inferences/s"},
+            "multi_gpu": {"profiling": "sharded round-robin over ranks, MIN all-reduce of costs (G1), "
+                                       "rank-0 selection broadcast (G2)" if world > 1 else "single GPU",
+                          "replica_outputs_identical": replicas_agree},
             "warm_l2_ms_per_step": warm_ms,
             "e2e": {"value": e2e_max, "unit": "ms", "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h},
             "gpu_launches": len(order) * args.steps,
