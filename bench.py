@@ -137,8 +137,28 @@ def oracle_baseline(graph, sel_cands, sel, budget_s=15.0):
         blas = max((x.get("num_threads", 1) for x in info), default=1)
     except Exception:
         blas = cores
-    return {"value": el / n * 1e3, "unit": "ms", "cores": int(blas), "host_cores": cores, "kind": "oracle",
-            "sample": f"{n} inferences of the selected orchestration (fp64 numpy, bf16/fp32 rounding at kernel outputs), {el:.1f} s"}
+    res = {"value": el / n * 1e3, "unit": "ms", "cores": int(blas), "host_cores": cores, "kind": "oracle",
+           "sample": f"{n} inferences of the selected orchestration (fp64 numpy, bf16/fp32 rounding at kernel outputs), {el:.1f} s"}
+    # SURVEY.md §8(d) oracle tasks: the same at one BLAS thread, and the unfissioned
+    # operator interpreter
+    from oracle.operators import eval_operator_graph
+
+    def timed(fn, budget):
+        k, t = 0, time.perf_counter()
+        while True:
+            fn()
+            k += 1
+            if time.perf_counter() - t > budget or k >= 2000:
+                return (time.perf_counter() - t) / k * 1e3, k
+    try:
+        import threadpoolctl
+        with threadpoolctl.threadpool_limits(1):
+            res["single_thread_ms"], _ = timed(
+                lambda: eval_orchestration(pg, sel_cands, sel, ins, G.topo_index, graph["dtype"]), budget_s / 3)
+    except Exception as e:
+        res["single_thread_ms"] = f"unavailable: {e}"[:120]
+    res["operator_interpreter_ms"], _ = timed(lambda: eval_operator_graph(graph, ins), budget_s / 3)
+    return res
 
 
 def time_plan(kg, sel, dev_in, steps=20, flush_mb=512):
@@ -230,27 +250,66 @@ def run_models(K, names, oracle_check=True):
     return res
 
 
-def scaled_variant(K, pk, batch=64, steps=10):
-    """C2 at batch 64 (M = 8192 tokens; SURVEY.md §8(d) C2 scale list): tune, select,
-    time; the dominant kernel re-timed cold against the tensor (or HBM) roofline."""
+def scaled_variant(K, pk, global_batch=64, steps=10, coll_dev=None):
+    """C2 at global batch 64 (M = 8192 tokens; SURVEY.md §8(d) C2 scale list) sharded over
+    the ranks (§8(e)): each rank tunes and selects for its LOCAL batch (reading A26), runs
+    its shard with no communication, and the step time is the max over ranks (G4); the
+    output shards are then all-gathered (G3, timed separately).  The dominant kernel is
+    re-timed cold against the tensor (or HBM) roofline."""
     import torch
+    import torch.distributed as dist
     from korch_workloads import make_inputs
+    from paper_2406_09465_b200.dist import (broadcast_selection, max_over_ranks, merge_costs, my_share, shard,
+                                            world)
+    rank, ws_, _ = world()
+    lo, hi = shard(global_batch, rank, ws_)
+    batch = hi - lo
     graph, cfg = config_graph("c2", batch)
     ctx = K.Context(torch.cuda.current_device())
     kg = K.KorchGraph(ctx, graph)
     cands = kg.enumerate(attention_pairs=True)
-    costs = kg.profile()
-    obj, sel = kg.select(costs)
-    ins = make_inputs(graph, seed=0)
+    t0 = time.perf_counter()
+    if ws_ > 1 and global_batch % ws_ == 0:
+        # equal shards -> identical graphs: profile a share each, MIN all-reduce (G1)
+        mine = my_share(len(cands), rank, ws_)
+        part = kg.profile(mine)
+        costs, variants = merge_costs(mine, part, [kg.variant_info(i)[1] for i in mine], len(cands),
+                                      device=coll_dev)
+        for i, v in enumerate(variants):
+            if v >= 0:
+                kg.set_variant(i, v)
+        obj, sel = kg.select(costs)
+        sel = broadcast_selection(sel, src=0, device=coll_dev)
+    else:
+        costs = kg.profile()
+        obj, sel = kg.select(costs)
+    t_tune = time.perf_counter() - t0
+    ins = make_inputs(graph, seed=1000 + rank)
     dev = K.torch_inputs(graph, {k: v[1] for k, v in ins.items()})
-    ms, _ = time_plan(kg, sel, dev, steps=steps)
+    if ws_ > 1:
+        dist.barrier()
+    ms, outs = time_plan(kg, sel, dev, steps=steps)
+    ms_max, = max_over_ranks([ms], device=coll_dev)
+    gather_ms = None
+    if ws_ > 1:
+        o = outs[0].contiguous() if coll_dev else outs[0].float().cpu()
+        bufs = [torch.empty_like(o) for _ in range(ws_)]
+        torch.cuda.synchronize()
+        t1 = time.perf_counter()
+        for _ in range(3):
+            dist.all_gather(bufs, o)
+        torch.cuda.synchronize()
+        gather_ms = (time.perf_counter() - t1) / 3 * 1e3
     order = kg.plan()
     dom = max(order, key=lambda i: costs[i])
     cold = kg.profile([dom], flush_l2=True, trials=7)[0]
     dc = cands[dom]
     flops = sum(cands[i]["flops"] for i in order)
-    res = {"workload": f"C2 ViT-B MHSA layer, batch {batch} x seq 128 (M = {batch * 128}), bf16",
-           "ms": ms, "kernels": len(order), "tflops_plan": flops / (ms * 1e-3) / 1e12,
+    res = {"workload": f"C2 ViT-B MHSA layer, global batch {global_batch} x seq 128 sharded over {ws_} GPU(s), "
+                       f"local batch {batch} (M = {batch * 128}), bf16",
+           "ms": ms_max, "ms_rank0": ms, "local_batch": batch, "kernels": len(order),
+           "throughput": {"value": global_batch / (ms_max * 1e-3), "unit": "sequences/s (seq 128)"},
+           "tflops_plan": flops / (ms * 1e-3) / 1e12, "tune_s": t_tune, "output_gather_ms_host_timed": gather_ms,
            "dominant": {"candidate": dom, "class": dc["klass"], "members": len(dc["members"]),
                         "ns_cold_l2": cold, "variant": kg.variant_info(dom)[2], "name": dc["signature"]}}
     if dc["flops"] > 0:
@@ -473,6 +532,11 @@ def main():
         dist.barrier()
     times = [a.elapsed_time(b) for a, b in ev]
     ms = statistics.mean(times)
+    qs = sorted(times)
+
+    def pct(q):
+        return qs[min(len(qs) - 1, int(round(q * (len(qs) - 1))))]
+    dist_ms = {"mean": ms, "median": statistics.median(times), "p10": pct(0.1), "p90": pct(0.9)}
 
     # warm back-to-back replays (context: the regime the profiler measures in)
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
@@ -533,6 +597,17 @@ def main():
                       "algorithmic_bytes": dc["bytes"], "flops": dc["flops"], "ns_cold_l2": dom_cold,
                       "ns_warm": costs[dom], "name": dc["signature"], "peak_source": pk["source"]}
 
+    # plan roofline: T*(u) = sum_i max(B_i / BW, F_i / P) over the selected
+    # kernels, and the launch floor n_kernels * t_min + T*(u), t_min = the cheapest profiled
+    # candidate of this graph (one launch of a near-empty kernel in graph replay)
+    t_star_ns = sum(max(cands[i]["bytes"] / pk["hbm_gbs"], cands[i]["flops"] / (pk["bf16_tflops"] * 1e3))
+                    for i in order)
+    t_min_ns = min(c for c in costs if c < K.INF)
+    plan_roof = {"t_star_us": t_star_ns / 1e3, "t_min_kernel_us": t_min_ns / 1e3,
+                 "floor_us": (len(order) * t_min_ns + t_star_ns) / 1e3,
+                 "frac_of_t_star": t_star_ns / (ms * 1e6), "frac_of_floor": (len(order) * t_min_ns + t_star_ns) / (ms * 1e6),
+                 "bytes": sum(cands[i]["bytes"] for i in order), "flops": sum(cands[i]["flops"] for i in order)}
+
     # gather max over ranks (G4): a step takes as long as its slowest rank
     from paper_2406_09465_b200.dist import max_over_ranks
     ms_max, e2e_max = max_over_ranks([ms, e2e_ms], device=coll_dev)
@@ -554,9 +629,9 @@ def main():
     if rank == 0 and world == 1 and args.models:
         models = run_models(K, [m for m in args.models.split(",") if m])
     scaled = None
-    if rank == 0 and world == 1 and not args.no_scaled and args.config == "c2":
+    if not args.no_scaled and args.config == "c2":
         try:
-            scaled = scaled_variant(K, pk)
+            scaled = scaled_variant(K, pk, coll_dev=coll_dev)
         except Exception as e:
             scaled = {"error": str(e)[:300]}
     bw = None
@@ -580,6 +655,8 @@ def main():
                                        "rank-0 selection broadcast (G2)" if world > 1 else "single GPU",
                           "replica_outputs_identical": replicas_agree},
             "warm_l2_ms_per_step": warm_ms,
+            "latency_ms_rank0": dist_ms,
+            "plan_roofline": plan_roof,
             "e2e": {"value": e2e_max, "unit": "ms", "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h},
             "gpu_launches": len(order) * args.steps,
             "kernels_per_step": len(order),
