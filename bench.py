@@ -231,6 +231,14 @@ def run_models(K, names, oracle_check=True):
                  "speedup_vs_operator_aligned": ms_base / ms_sel,
                  "blp_objective_ns": obj, "operator_aligned_objective_ns": sum(costs[i] for i in base),
                  "tuning_s": {"enumerate": t_enum, "compile": t_comp, "profile": t_prof, "select": t_sel}}
+        kinds = {n["id"]: n["kind"] for n in kg.prim["nodes"]}
+
+        def top(plan, n=6):
+            return [{"cand": i, "ns": costs[i], "class": cands[i]["klass"], "bytes": cands[i]["bytes"],
+                     "flops": cands[i]["flops"], "kinds": [kinds[m] for m in cands[i]["members"]],
+                     "variant": kg.variant_info(i)[2]} for i in sorted(plan, key=lambda i: -costs[i])[:n]]
+        entry["slowest_selected"] = top(sel)
+        entry["slowest_operator_aligned"] = top(base)
         if oracle_check:
             from oracle.enumeration import PGraph
             from oracle.evaluate import eval_orchestration

@@ -158,6 +158,72 @@ def test_layout_only_bit_exact(ctx, dtype):
         c.check(c.completion([i]), exact=True)
 
 
+def _every_variant(c, idx, exact):
+    for i in idx:
+        nv, _, _ = c.kg.variant_info(i)
+        for v in range(nv):
+            c.kg.set_variant(i, v)
+            c.check(c.completion([i]), exact=exact)
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("dtype", ["f32", "bf16"])
+def test_layout_every_variant_bit_exact(ctx, dtype):
+    """Every launch variant, including the shared-memory staged tiles (TR), of every
+    candidate of the layout graph: bit-exact."""
+    c = Case(ctx, _layout_graph(dtype))
+    tiles = 0
+    for x in c.cands:
+        if x["klass"] == "rejected":
+            continue
+        nv = c.kg.variant_info(x["index"])[0]
+        for v in range(nv):
+            c.kg.set_variant(x["index"], v)
+            tiles += "tile" in c.kg.variant_info(x["index"])[2]
+    assert tiles > 0
+    _every_variant(c, [x["index"] for x in c.cands if x["klass"] != "rejected"], exact=True)
+
+
+def _transpose_chain(dtype, n, a, b):
+    """Ragged transposes (tile edges in both axes) feeding elementwise work, and an
+    NCHW <-> tokens round trip with a reflect pad (guarded staged loads)."""
+    gb = GraphBuilder(dtype)
+    x = gb.input("x", [n, a, b])
+    r = gb.input("r", [n, b, a])
+    bias = gb.input("bias", [a], std=0.1)
+    y = gb.op("Transpose", x, perm=[0, 2, 1])               # [n, b, a]
+    y = gb.op("Add", y, r)
+    y = gb.op("Add", y, bias)
+    y = gb.op("GELU", y)
+    z = gb.op("Reshape", y, shape=[n, b, a, 1])
+    z = gb.op("Transpose", z, perm=[0, 2, 1, 3])            # [n, a, b, 1]
+    z = gb.op("Pad", z, pads=[[0, 0], [0, 0], [1, 1], [0, 0]], mode="reflect")
+    z = gb.op("Relu", z)
+    gb.output(z)
+    return gb.build()
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("dtype", ["f32", "bf16"])
+@pytest.mark.parametrize("n,a,b", [(1, 64, 96), (2, 45, 70), (3, 130, 33)])
+def test_transpose_tiles_every_variant(ctx, dtype, n, a, b):
+    c = Case(ctx, _transpose_chain(dtype, n, a, b))
+    idx = [x["index"] for x in c.cands if x["klass"] in ("pw", "rr")]
+    assert any("tile" in _tags(c, i) for i in idx)
+    _every_variant(c, idx, exact=False)
+
+
+def _tags(c, i):
+    nv, ch, _ = c.kg.variant_info(i)
+    t = []
+    for v in range(nv):
+        c.kg.set_variant(i, v)
+        t.append(c.kg.variant_info(i)[2])
+    if ch >= 0:
+        c.kg.set_variant(i, ch)
+    return " ".join(t)
+
+
 @pytest.mark.gpu
 def test_misc_memory_bound_ops(ctx):
     b = GraphBuilder("f32")
