@@ -50,6 +50,28 @@ Lin ExprCtx::code(const std::string& c, int64_t lo, int64_t hi) const {
   return from_atom(a);
 }
 
+// c*k*(X / c) + k*(X % c) == k*X (non-negative X): folds the index arithmetic that a
+// reshape followed by its inverse leaves behind (e.g. a row axis merged from two axes).
+static Lin recombine(const Lin& r) {
+  for (size_t i = 0; i < r.terms.size(); ++i) {
+    const Atom& d = r.terms[i].second;
+    if (d.type != Atom::Div || r.terms[i].first % d.c) continue;
+    const int64_t k = r.terms[i].first / d.c;
+    const std::string sk = d.sub->key();
+    for (size_t j = 0; j < r.terms.size(); ++j) {
+      const Atom& m = r.terms[j].second;
+      if (j == i || m.type != Atom::Mod || m.c != d.c || r.terms[j].first != k || m.sub->key() != sk) continue;
+      if (d.sub->lo() < 0) continue;
+      Lin rest;
+      rest.c0 = r.c0;
+      for (size_t t = 0; t < r.terms.size(); ++t)
+        if (t != i && t != j) rest.terms.push_back(r.terms[t]);
+      return ExprCtx::add(rest, ExprCtx::scale(*d.sub, k));
+    }
+  }
+  return r;
+}
+
 Lin ExprCtx::add(const Lin& a, const Lin& b) {
   Lin r;
   r.c0 = a.c0 + b.c0;
@@ -65,7 +87,7 @@ Lin ExprCtx::add(const Lin& a, const Lin& b) {
       ++i, ++j;
     }
   }
-  return r;
+  return recombine(r);
 }
 
 Lin ExprCtx::scale(const Lin& a, int64_t k) {

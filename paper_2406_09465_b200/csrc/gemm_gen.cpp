@@ -107,6 +107,21 @@ std::string str(int64_t v) { return std::to_string(v); }
 // the canonical MN-major 128B-swizzled shared-memory layout (zero padding, strides and the
 // K tail as predicated loads), published to the tensor core with fence.proxy.async and an
 // mbarrier; one thread issues the MMAs; the fused epilogue is the GEMM template's.
+// The B operand of a gather GEMM: element (k, p) of the [K, NP] operand is read from
+// external tensor `src` by the code in `elem` (defines `ok` and `idx` from kg, p).
+struct GatherSpec {
+  Ref a_src, b_src;
+  int64_t M = 0, NP = 0, K = 0;
+  int64_t a_off = 0, a_row = 0;   // A = [M, K] K-major view: element offset, row stride (elements)
+  std::string elem;               // per-element gather code
+  std::string prologue;           // per-k code shared by the 8 elements of a group
+  std::string tag;
+  std::string prefix;             // kernel name prefix
+  int64_t b_bytes = 0;            // algorithmic bytes of B
+};
+
+static KernelPlan generate_gather_gemm(const Graph& g, const Candidate& c, int mm, const GatherSpec& gs);
+
 static KernelPlan generate_conv_gemm(const Graph& g, const Candidate& c, int mm) {
   KernelPlan kp;
   kp.klass = KORCH_CLASS_REJECTED;
@@ -132,7 +147,77 @@ static KernelPlan generate_conv_gemm(const Graph& g, const Candidate& c, int mm)
   int64_t Cin = xs[1], H = xs[2], W = xs[3], F = ws[0], R = ws[2], S = ws[3];
   int64_t K = Cin * R * S, OH = ys[2], OW = ys[3], NP = ys[0] * OH * OW;
   if (K % 8) { kp.reject = "conv K = C*R*S not a multiple of 8 (TMA row stride)"; return kp; }
-  std::vector<Ref> pre{wr, xr};
+  GatherSpec gs;
+  gs.a_src = wr;
+  gs.b_src = xr;
+  gs.M = F;
+  gs.NP = NP;
+  gs.K = K;
+  gs.a_off = 0;
+  gs.a_row = K;
+  std::ostringstream pr, el;
+  pr << "        const int ci = kg / " << R * S << ", rs = kg % " << R * S << ";\n";
+  pr << "        const int rr = rs / " << S << ", ss = rs % " << S << ";\n";
+  el << "          const int img = p / " << OH * OW << ", q = p % " << OH * OW << ";\n";
+  el << "          const int ih = (q / " << OW << ") * " << L.stride[0] << " + rr - " << L.cpad[0] << ";\n";
+  el << "          const int iw = (q % " << OW << ") * " << L.stride[1] << " + ss - " << L.cpad[1] << ";\n";
+  el << "          const bool ok = kg < " << K << " && p < " << NP << " && (unsigned)ih < " << H << "u && (unsigned)iw < "
+     << W << "u;\n";
+  el << "          const size_t idx = (((size_t)img * " << Cin << " + ci) * " << H << " + ih) * " << W << " + iw;\n";
+  gs.prologue = pr.str();
+  gs.elem = el.str();
+  std::ostringstream t;
+  t << "conv-igemm F=" << F << " P=" << NP << " K=" << K << " (" << R << "x" << S << " s" << L.stride[0] << ")";
+  gs.tag = t.str();
+  gs.prefix = "korch_conv_";
+  gs.b_bytes = 2 * numel(xs);
+  return generate_gather_gemm(g, c, mm, gs);
+}
+
+// KB5 fallback for a 2-D MatMul whose B view has no 16-byte-aligned stride (e.g. a
+// pointwise conv over H*W = 196 tokens): A by TMA, B gathered by the conv template's
+// producer warps.
+static KernelPlan generate_matmul_gather(const Graph& g, const Candidate& c, int mm, const View& va, const View& vb) {
+  KernelPlan kp;
+  kp.klass = KORCH_CLASS_REJECTED;
+  const Prim& L = g.prims[mm];
+  const Shape& C = L.shape;
+  for (size_t i = 0; i + 2 < C.size(); ++i)
+    if (C[i] != 1) { kp.reject = "gather GEMM: batched"; return kp; }
+  const int nbA = (int)va.shape.size() - 2, nbB = (int)vb.shape.size() - 2;
+  const int64_t M = C[C.size() - 2], N = C.back(), K = va.shape.back();
+  if (va.coef[nbA + 1] != 1 || (va.off * 2) % 16 || (va.coef[nbA] * 2) % 16 || va.coef[nbA] <= 0 || K % 8) {
+    kp.reject = "gather GEMM: A not a 16-byte aligned K-major view";
+    return kp;
+  }
+  GatherSpec gs;
+  gs.a_src = va.src;
+  gs.b_src = vb.src;
+  gs.M = M;
+  gs.NP = N;
+  gs.K = K;
+  gs.a_off = va.off;
+  gs.a_row = va.coef[nbA];
+  std::ostringstream el;
+  el << "          const bool ok = kg < " << K << " && p < " << N << ";\n";
+  el << "          const size_t idx = " << vb.off << " + (size_t)kg * " << vb.coef[nbB] << " + (size_t)p * " << vb.coef[nbB + 1]
+     << ";\n";
+  gs.elem = el.str();
+  std::ostringstream t;
+  t << "gemm-gatherB M=" << M << " N=" << N << " K=" << K;
+  gs.tag = t.str();
+  gs.prefix = "korch_gg_";
+  gs.b_bytes = 2 * numel(vb.shape);
+  return generate_gather_gemm(g, c, mm, gs);
+}
+
+static KernelPlan generate_gather_gemm(const Graph& g, const Candidate& c, int mm, const GatherSpec& gs) {
+  KernelPlan kp;
+  kp.klass = KORCH_CLASS_REJECTED;
+  for (int m : c.members)
+    if (g.prims[m].kind == Kind::Reduce) { kp.reject = "gather GEMM: no in-tile row reductions"; return kp; }
+  const int64_t F = gs.M, NP = gs.NP, K = gs.K;
+  std::vector<Ref> pre{gs.a_src, gs.b_src};
   GemmEpilogue ep0;
   std::string err;
   if (!make_gemm_epilogue(g, c, mm, 32, pre, &ep0, &err)) {
@@ -140,9 +225,9 @@ static KernelPlan generate_conv_gemm(const Graph& g, const Candidate& c, int mm)
     return kp;
   }
   kp.ext = ep0.ext;
-  const int slotW = 0, slotX = 1;
+  const int slotW = 0, slotX = (gs.a_src.is_input == gs.b_src.is_input && gs.a_src.id == gs.b_src.id) ? 0 : 1;
   kp.flops = 2.0 * (double)F * (double)NP * (double)K;
-  kp.bytes = ep0.bytes + 2 * (F * K + numel(xs));
+  kp.bytes = ep0.bytes + 2 * F * K + gs.b_bytes;
   const int64_t NK = (K + 63) / 64, Mt = (F + 127) / 128;
   for (int BN : {64, 128}) {
     GemmEpilogue ep;
@@ -158,10 +243,10 @@ static KernelPlan generate_conv_gemm(const Graph& g, const Candidate& c, int mm)
     da.tensor = slotW;
     da.dtype = 1;
     da.swizzle = 3;
-    da.elem_off = 0;
+    da.elem_off = gs.a_off;
     da.rank = 2;
     da.dims[0] = K; da.strides[0] = 2; da.box[0] = 64;
-    da.dims[1] = F; da.strides[1] = K * 2; da.box[1] = 128;
+    da.dims[1] = F; da.strides[1] = gs.a_row * 2; da.box[1] = 128;
     std::ostringstream k;
     k << "extern \"C\" __global__ void __launch_bounds__(192, 1) KNAME(";
     for (size_t i = 0; i < kp.ext.size(); ++i)
@@ -194,18 +279,12 @@ static KernelPlan generate_conv_gemm(const Graph& g, const Candidate& c, int mm)
     k << "      for (int u = threadIdx.x; u < " << 64 * (BN / 8) << "; u += 128) {\n";
     k << "        const int kk = u / " << BN / 8 << ", grp = u % " << BN / 8 << ";\n";
     k << "        const int kg = kb * 64 + kk;\n";
-    k << "        const int ci = kg / " << R * S << ", rs = kg % " << R * S << ";\n";
-    k << "        const int rr = rs / " << S << ", ss = rs % " << S << ";\n";
+    k << gs.prologue;
     k << "        unsigned short v[8];\n";
     k << "        #pragma unroll\n        for (int e = 0; e < 8; ++e) {\n";
     k << "          const int p = tile_n + grp * 8 + e;\n";
-    k << "          const int img = p / " << OH * OW << ", q = p % " << OH * OW << ";\n";
-    k << "          const int ih = (q / " << OW << ") * " << L.stride[0] << " + rr - " << L.cpad[0] << ";\n";
-    k << "          const int iw = (q % " << OW << ") * " << L.stride[1] << " + ss - " << L.cpad[1] << ";\n";
-    k << "          const bool ok = kg < " << K << " && p < " << NP << " && (unsigned)ih < " << H << "u && (unsigned)iw < "
-      << W << "u;\n";
-    k << "          v[e] = ok ? __ldg(xin + (((size_t)img * " << Cin << " + ci) * " << H << " + ih) * " << W
-      << " + iw) : (unsigned short)0;\n";
+    k << gs.elem;
+    k << "          v[e] = ok ? __ldg(xin + idx) : (unsigned short)0;\n";
     k << "        }\n";
     k << "        uint4 pk;\n";
     k << "        pk.x = v[0] | ((unsigned)v[1] << 16); pk.y = v[2] | ((unsigned)v[3] << 16);\n";
@@ -254,7 +333,7 @@ static KernelPlan generate_conv_gemm(const Graph& g, const Candidate& c, int mm)
     KernelVariant kv;
     std::string src = k.str();
     char nm[64];
-    std::snprintf(nm, sizeof nm, "korch_conv_%016llx",
+    std::snprintf(nm, sizeof nm, "%s%016llx", gs.prefix.c_str(),
                   (unsigned long long)fnv1a(std::string(kSm100GemmTemplate) + "\n" + src));
     kv.name = nm;
     size_t pos = src.find("KNAME");
@@ -268,8 +347,7 @@ static KernelPlan generate_conv_gemm(const Graph& g, const Candidate& c, int mm)
     kv.smem = smem;
     kv.tma = {da};
     std::ostringstream t;
-    t << "conv-igemm BM=128 BN=" << BN << " BK=64 stages=" << S_ << " F=" << F << " P=" << NP << " K=" << K
-      << " (" << R << "x" << S << " s" << L.stride[0] << ")";
+    t << gs.tag << " BM=128 BN=" << BN << " BK=64 stages=" << S_;
     kv.tag = t.str();
     kp.variants.push_back(kv);
   }
@@ -412,6 +490,7 @@ KernelPlan generate_gemm(const Graph& g, const Candidate& c) {
         cfgs.push_back({bn, ks});
       }
   }
+  bool gather_fallback = false;
   for (const Cfg& cf : cfgs) {
     const int BN = cf.bn, KS = cf.ks;
     // epilogue chunk (TMEM columns per pass); the whole row when reducing
@@ -431,6 +510,7 @@ KernelPlan generate_gemm(const Graph& g, const Candidate& c) {
                        : build_desc(vb, slotB, N, K, b_k, (uint32_t)bmn_box, 64, nbB, &bb_axes, &db));
     if (!ok) {
       kp.reject = "operand strides not expressible as a TMA tensor map";
+      gather_fallback = true;
       continue;
     }
     if (!b_kmaj) db.swizzle = b_swz_tma;
@@ -605,7 +685,14 @@ KernelPlan generate_gemm(const Graph& g, const Candidate& c) {
     kv.tag = t.str();
     kp.variants.push_back(kv);
   }
-  if (kp.variants.empty()) return kp;
+  if (kp.variants.empty()) {
+    if (gather_fallback) {
+      KernelPlan gp = generate_matmul_gather(g, c, mm, va, vb);
+      if (gp.klass != KORCH_CLASS_REJECTED) return gp;
+      kp.reject += "; " + gp.reject;
+    }
+    return kp;
+  }
   kp.klass = KORCH_CLASS_GEMM;
   kp.reject.clear();
   return kp;

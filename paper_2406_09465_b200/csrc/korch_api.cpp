@@ -305,7 +305,12 @@ static void compile_many(korch_graph* G, const std::vector<int64_t>& idx, int th
       batches.emplace_back();
     batches.back().push_back(j);
   }
-  if (threads <= 0) threads = (int)std::max(1u, std::thread::hardware_concurrency());
+  if (threads <= 0) {
+    // NVRTC holds ~0.5-1 GB per in-flight tcgen05 batch: bound the parallelism
+    const char* e = getenv("KORCH_COMPILE_THREADS");
+    threads = e ? atoi(e) : (int)std::min(24u, std::max(1u, std::thread::hardware_concurrency()));
+    if (threads <= 0) threads = 1;
+  }
   threads = std::min<int>(threads, (int)std::max<size_t>(1, batches.size()));
   std::atomic<size_t> next{0};
   auto worker = [&] {

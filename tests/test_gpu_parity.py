@@ -213,6 +213,32 @@ def test_transpose_tiles_every_variant(ctx, dtype, n, a, b):
     _every_variant(c, idx, exact=False)
 
 
+def _column_graph(kind, dtype, shape, axis):
+    gb = GraphBuilder(dtype)
+    x = gb.input("x", shape)
+    if kind == "Softmax":
+        y = gb.op("Softmax", gb.op("MulC", x, c=0.5), axis=axis)     # reduce + broadcast back
+    else:
+        y = gb.op("Relu", gb.op(kind, gb.op("Neg", x), axis=axis))
+    gb.output(y)
+    return gb.build()
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("kind,dtype,shape,axis", [("ReduceSum", "f32", [200, 96], 0),
+                                                   ("ReduceMean", "bf16", [3, 70, 50], 1),
+                                                   ("ReduceMax", "f32", [130, 2, 33], 0),
+                                                   ("Softmax", "f32", [64, 100], 0),
+                                                   ("Softmax", "bf16", [2, 96, 40], 1)])
+def test_column_reductions_every_variant(ctx, kind, dtype, shape, axis):
+    """Reductions along a non-innermost axis: every variant, including the column mapping
+    (CR: lanes over consecutive rows, shared-memory row combine, ragged row blocks)."""
+    c = Case(ctx, _column_graph(kind, dtype, shape, axis))
+    idx = [x["index"] for x in c.cands if x["klass"] == "rr"]
+    assert any("col" in _tags(c, i) for i in idx)
+    _every_variant(c, idx, exact=False)
+
+
 def _tags(c, i):
     nv, ch, _ = c.kg.variant_info(i)
     t = []
@@ -391,7 +417,8 @@ def _gemm_graph(m, k, n, batch=1, act="Relu"):
 
 
 @pytest.mark.gpu
-@pytest.mark.parametrize("m,k,n,batch", [(128, 768, 768, 1), (128, 768, 2304, 1), (200, 512, 256, 2)])
+@pytest.mark.parametrize("m,k,n,batch", [(128, 768, 768, 1), (128, 768, 2304, 1), (200, 512, 256, 2),
+                                         (128, 256, 196, 1), (160, 64, 676, 1), (64, 128, 100, 1)])
 def test_every_gemm_variant(ctx, m, k, n, batch):
     """Every launch variant (tile width, split-K with the self-cleaning scratch) of every
     GEMM candidate; each plan executes twice and both results must match the oracle (a
