@@ -230,6 +230,7 @@ def run_models(K, names, oracle_check=True):
                  "operator_aligned_ms": ms_base, "operator_aligned_kernels": len(base),
                  "speedup_vs_operator_aligned": ms_base / ms_sel,
                  "blp_objective_ns": obj, "operator_aligned_objective_ns": sum(costs[i] for i in base),
+                 "compile_failures": len(kg.compile_failures),
                  "tuning_s": {"enumerate": t_enum, "compile": t_comp, "profile": t_prof, "select": t_sel}}
         kinds = {n["id"]: n["kind"] for n in kg.prim["nodes"]}
 
@@ -318,6 +319,7 @@ def scaled_variant(K, pk, global_batch=64, steps=10, coll_dev=None):
            "ms": ms_max, "ms_rank0": ms, "local_batch": batch, "kernels": len(order),
            "throughput": {"value": global_batch / (ms_max * 1e-3), "unit": "sequences/s (seq 128)"},
            "tflops_plan": flops / (ms * 1e-3) / 1e12, "tune_s": t_tune, "output_gather_ms_host_timed": gather_ms,
+           "plan_members": [cands[i]["members"] for i in order],
            "dominant": {"candidate": dom, "class": dc["klass"], "members": len(dc["members"]),
                         "ns_cold_l2": cold, "variant": kg.variant_info(dom)[2], "name": dc["signature"]}}
     if dc["flops"] > 0:
@@ -640,6 +642,9 @@ def main():
     if not args.no_scaled and args.config == "c2":
         try:
             scaled = scaled_variant(K, pk, coll_dev=coll_dev)
+            # P:610-620 / SURVEY N3: is the optimal orchestration batch dependent?
+            scaled["plan_differs_from_bs1"] = sorted(scaled["plan_members"]) != sorted(cands[i]["members"]
+                                                                                       for i in order)
         except Exception as e:
             scaled = {"error": str(e)[:300]}
     bw = None

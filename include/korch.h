@@ -148,7 +148,10 @@ korch_status korch_candidate_source(korch_graph* g, int64_t i, char* buf, size_t
 
 /* Generate and compile (NVRTC, -arch=sm_100a) candidates idx[0..n).  Works on
  * host-only contexts (no GPU needed).  cache_dir (may be NULL) holds cubins keyed
- * by source hash.  ok[k] (caller-owned, n entries, may be NULL) = 1 on success. */
+ * by source hash.  ok[k] (caller-owned, n entries, may be NULL) = 1 when at least
+ * one launch variant of candidate idx[k] compiled (variants that fail are dropped).
+ * Returns KORCH_E_NVRTC (message = first compiler log) when a generable candidate
+ * has no compiled variant; ok[] is filled either way. */
 korch_status korch_compile(korch_graph* g, const int64_t* idx, int64_t n, int32_t threads,
                            const char* cache_dir, int32_t* ok);
 

@@ -331,4 +331,6 @@ def o_n(size):
     return sum((size // s) ** 2 for s in (8, 16, 32))
 
 
-MODELS = {"candy": candy, "segformer": segformer, "efficientvit": efficientvit, "yolox": yolox_nano}
+MODELS = {"candy": candy, "segformer": segformer, "efficientvit": efficientvit, "yolox": yolox_nano,
+          # the paper's EfficientViT resolution (reading A22), 1024:1 K^T V at stage 3
+          "efficientvit2048": lambda: efficientvit(size=2048)}

@@ -22,6 +22,7 @@ ERRORS = {
     -5: "KORCH_E_STATE_EXPLOSION", -6: "KORCH_E_INFEASIBLE", -7: "KORCH_E_NOT_SCHEDULABLE",
     -8: "KORCH_E_NVRTC", -9: "KORCH_E_CUDA", -10: "KORCH_E_OOM", -11: "KORCH_E_UNSUPPORTED",
 }
+KORCH_E_NVRTC = -8
 CLASS_NAMES = {0: "rejected", 1: "pw", 2: "rr", 3: "gemm"}
 INT64_MAX = (1 << 63) - 1
 

@@ -126,8 +126,16 @@ class KorchGraph:
         arr = _lib.i64_array(idx)
         ok = (C.c_int32 * max(1, len(idx)))()
         cd = cache_dir.encode() if cache_dir else None
-        check(LIB.korch_compile(self.h, arr, len(idx), threads, cd, ok))
-        return [ok[k] for k in range(len(idx))]
+        st = LIB.korch_compile(self.h, arr, len(idx), threads, cd, ok)
+        flags = [ok[k] for k in range(len(idx))]
+        if st == _lib.KORCH_E_NVRTC:
+            # candidates with no compiled variant are "cannot be generated": the
+            # profiler gives them cost INF; the failures are kept for inspection
+            self.compile_failures = [(i, LIB.korch_last_error().decode()) for i, f in zip(idx, flags) if not f]
+        else:
+            check(st)
+            self.compile_failures = []
+        return flags
 
     def profile(self, idx=None, warmup=3, launches=20, trials=5, flush_l2=False, tune=True,
                 compile_threads=0):

@@ -601,13 +601,13 @@ korch_status korch_compile(korch_graph* G, const int64_t* idx, int64_t n, int32_
     std::string first_err;
     for (int64_t k = 0; k < n; ++k) {
       const CandState& s = G->cs[v[k]];
-      bool good = s.plan.klass != KORCH_CLASS_REJECTED;
+      // a launch variant that fails to compile is dropped (the profiler skips it); the
+      // candidate is generable while at least one variant compiled
+      bool good = false;
       for (auto& var : s.plan.variants) {
         Module* m = G->ctx->module_for(var.name);
-        if (!m->compiled) {
-          good = false;
-          if (first_err.empty()) first_err = var.name + ": " + m->log;
-        }
+        if (m->compiled) good = true;
+        else if (first_err.empty()) first_err = var.name + ": " + m->log;
       }
       if (ok) ok[k] = good ? 1 : 0;
       if (s.plan.klass != KORCH_CLASS_REJECTED && !good) all_ok = false;

@@ -239,6 +239,39 @@ def test_column_reductions_every_variant(ctx, kind, dtype, shape, axis):
     _every_variant(c, idx, exact=False)
 
 
+def _contraction_graph(dtype, batch, tokens, d):
+    """EfficientViT's K^T V at a large token:d ratio: K = tokens, N = d + 1."""
+    gb = GraphBuilder(dtype)
+    k = gb.input("k", [batch, tokens, d])
+    v = gb.input("v", [batch, tokens, d + 1])
+    kt = gb.op("Transpose", gb.op("Relu", k), perm=[0, 2, 1])
+    y = gb.op("MatMul", kt, v)
+    gb.output(gb.op("MulC", y, c=1.0 / tokens))
+    return gb.build()
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("dtype", ["f32", "bf16"])
+def test_large_k_contraction_as_row_reduction(ctx, dtype):
+    c = Case(ctx, _contraction_graph(dtype, 2, 8192, 16))
+    gen = [x["index"] for x in c.cands if x["klass"] != "rejected"]
+    assert any(len(x["members"]) >= 3 and x["klass"] == "rr" for x in c.cands)
+    _every_variant(c, gen, exact=False)
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("dtype", ["f32", "bf16"])
+def test_long_elementwise_rows_chunked(ctx, dtype):
+    """Rows longer than the register tile (L = 20480) are cut into chunks."""
+    gb = GraphBuilder(dtype)
+    x = gb.input("x", [2, 3, 20480])
+    gb.output(gb.op("GELU", gb.op("Add", x, gb.input("b", [20480], std=0.1))))
+    c = Case(ctx, gb.build())
+    gen = [x["index"] for x in c.cands if x["klass"] != "rejected"]
+    assert len(gen) == len(c.cands)
+    _every_variant(c, gen, exact=False)
+
+
 def _tags(c, i):
     nv, ch, _ = c.kg.variant_info(i)
     t = []
