@@ -62,6 +62,18 @@ struct GemmEpilogue {
 // `store` holds the name of the float[cw] array with its values (no global store).
 bool make_gemm_epilogue(const Graph& g, const Candidate& c, int mm, int cw, const std::vector<Ref>& pre_ext,
                         GemmEpilogue* out, std::string* err, int target = -1);
+// Prologue of a GEMM whose A operand is computed in the kernel (e.g. LayerNorm feeding a
+// Linear): `body` runs once per A row (local row r, global row gm; one warp per row,
+// lane = tid) and writes the bf16 row into the resident, 128B-swizzled K-major A tile at
+// shared address `sA`.
+struct GemmPrologue {
+  std::vector<Ref> ext;               // pre_ext first, then prologue operands
+  std::string body;
+  int64_t bytes = 0;                  // prologue reads (the A tile never reaches HBM)
+  std::vector<std::string> batch_vars;
+};
+bool make_gemm_prologue(const Graph& g, const Candidate& c, int mm, const std::vector<Ref>& pre_ext,
+                        GemmPrologue* out, std::string* err);
 KernelPlan generate_attention(const Graph& g, const Candidate& c);   // gemm_gen.cpp (N2)
 KernelPlan generate_gemm(const Graph& g, const Candidate& c);   // gemm_gen.cpp
 std::string kernel_prelude();

@@ -358,6 +358,204 @@ static KernelPlan generate_gather_gemm(const Graph& g, const Candidate& c, int m
   return kp;
 }
 
+// KB5-P: GEMM with a computed A operand (a LayerNorm / elementwise chain over K feeding
+// the Linear, P:433-435's "memory-intensive + compute-intensive" fusion that library GEMMs
+// cannot do).  The CTA's whole A row block [128 x K] stays resident in shared memory:
+// warps 0-3 compute it row by row with the row-template emitter (one warp per row,
+// shuffle reductions over K, 16-byte loads) and store bf16 straight into the canonical
+// K-major 128B-swizzled layout; warp 4 streams B by TMA through a stage ring; warp 5
+// issues tcgen05.mma once A is published (fence.proxy.async + mbarrier); warps 0-3 then
+// run the fused epilogue from TMEM.  K <= 768 (A tile <= 192 KB).
+static KernelPlan generate_prologue_gemm(const Graph& g, const Candidate& c, int mm) {
+  KernelPlan kp;
+  kp.klass = KORCH_CLASS_REJECTED;
+  const Prim& L = g.prims[mm];
+  std::set<int> mem(c.members.begin(), c.members.end());
+  View vb;
+  std::set<int> chainB;
+  std::string err;
+  if (L.kind != Kind::MatMul) { kp.reject = "prologue GEMM: MatMul only"; return kp; }
+  if (!operand_view(g, mem, L, 1, &vb, &chainB, &err)) { kp.reject = "prologue GEMM B: " + err; return kp; }
+  if (g.dtype_of(vb.src) != DType::BF16) { kp.reject = "prologue GEMM: B must be bf16"; return kp; }
+  for (int m : c.members)
+    if (g.prims[m].kind == Kind::Reduce && g.topo_index[m] > g.topo_index[mm]) {
+      kp.reject = "prologue GEMM: no epilogue reductions";
+      return kp;
+    }
+  const Shape& C = L.shape;
+  const int nbC = (int)C.size() - 2;
+  const Shape& as = g.shape_of(L.in[0]);
+  const int64_t M = C[nbC], N = C[nbC + 1], K = as.back();
+  const int nbB = (int)vb.shape.size() - 2;
+  if ((int)as.size() - 2 != nbC || (nbB != 0 && nbB != nbC)) { kp.reject = "prologue GEMM: batch layout"; return kp; }
+  if (K % 64 || K > 768) { kp.reject = "prologue GEMM: K % 64 != 0 or K > 768"; return kp; }
+  const int64_t b_k = vb.coef[nbB], b_n = vb.coef[nbB + 1];
+  const bool b_kmaj = b_k == 1, b_nmaj = !b_kmaj && (b_n == 1 || N == 1);
+  if (!(b_kmaj || b_nmaj) || (vb.off * 2) % 16) { kp.reject = "prologue GEMM: B not TMA-able"; return kp; }
+  GemmPrologue pro;
+  std::vector<Ref> pre{vb.src};
+  if (!make_gemm_prologue(g, c, mm, pre, &pro, &err)) { kp.reject = "prologue: " + err; return kp; }
+  const int64_t NKA = K / 64;
+  const int A_RES = (int)(NKA * 16384);
+  int64_t batch = 1;
+  for (int b = 0; b < nbC; ++b) batch *= C[b];
+  kp.flops = 2.0 * (double)M * (double)N * (double)K * (double)batch;
+  for (int BN : {16, 32, 64, 128}) {
+    if (BN > 64 && BN / 2 >= N) continue;
+    const int CW = BN < 32 ? BN : 32;
+    GemmEpilogue ep;
+    if (!make_gemm_epilogue(g, c, mm, CW, pro.ext, &ep, &err)) { kp.reject = err; continue; }
+    const int B_BYTES = BN * 64 * 2;
+    const int budget = 227 * 1024 - A_RES - 1024 - 256;
+    const int S = (int)std::min<int64_t>(NKA, budget / B_BYTES);
+    if (S < 2) { kp.reject = "prologue GEMM: shared memory"; continue; }
+    const int smem = A_RES + S * B_BYTES + 1024 + (2 * S + 2) * 8 + 16;
+    const int tcols = BN < 32 ? 32 : BN;
+    const int64_t Mt = (M + 127) / 128, Nt = (N + BN - 1) / BN;
+    const int bmn_box = BN < 64 ? BN : 64;
+    const int b_swz_tma = bmn_box == 64 ? 3 : bmn_box == 32 ? 2 : 1;
+    const int b_swz_umma = bmn_box == 64 ? 2 : bmn_box == 32 ? 4 : 6;
+    const int b_row_bytes = bmn_box * 2;
+    TmaDesc db;
+    std::vector<int> bb_axes;
+    {
+      db.tensor = 0;
+      db.dtype = 1;
+      db.swizzle = 3;
+      db.elem_off = vb.off;
+      db.rank = 0;
+      auto push = [&](int64_t dim, int64_t st, uint32_t box) {
+        db.dims[db.rank] = dim; db.strides[db.rank] = st * 2; db.box[db.rank] = box; db.rank++;
+      };
+      if (b_kmaj) { push(K, 1, 64); push(N, N > 1 ? b_n : K, (uint32_t)BN); }
+      else { push(N, 1, (uint32_t)bmn_box); push(K, b_k, 64); db.swizzle = b_swz_tma; }
+      bool ok = true;
+      for (int b = 0; b < nbB; ++b)
+        if (vb.coef[b] != 0 && vb.shape[b] > 1) {
+          if (db.rank >= 5) ok = false;
+          else { push(vb.shape[b], vb.coef[b], 1); bb_axes.push_back(b); }
+        }
+      for (int i = 1; i < db.rank; ++i)
+        if (db.strides[i] % 16 || db.strides[i] <= 0) ok = false;
+      if (!ok) { kp.reject = "prologue GEMM: B strides not TMA-able"; continue; }
+    }
+    const uint32_t idesc = (1u << 4) | (1u << 7) | (1u << 10) | ((b_kmaj ? 0u : 1u) << 16) |
+                           ((uint32_t)(BN >> 3) << 17) | ((uint32_t)(128 >> 4) << 24);
+    auto coords = [&](const std::string& inner, const std::string& outer) {
+      std::string s2 = inner + ", " + outer;
+      for (int b : bb_axes) s2 += ", " + ep.batch_vars[b];
+      return s2;
+    };
+    const std::string load = "tma_load_" + std::to_string(db.rank) + "d";
+    std::ostringstream k;
+    k << "extern \"C\" __global__ void __launch_bounds__(192, 1) KNAME(";
+    for (size_t i = 0; i < ep.ext.size(); ++i)
+      k << "const " << (g.dtype_of(ep.ext[i]) == DType::F32 ? "float" : "bf16_t") << "* __restrict__ p" << i << ", ";
+    k << (g.prims[c.output].dtype == DType::F32 ? "float" : "bf16_t") << "* __restrict__ out, "
+      << "const __grid_constant__ TmaMap tmB) {\n";
+    k << "  typedef " << (numel(C) >= (1LL << 31) ? "long long" : "int") << " idx_t;\n";
+    k << "  extern __shared__ __align__(1024) unsigned char smem_raw[];\n";
+    k << "  unsigned char* smem = (unsigned char*)(((unsigned long long)smem_raw + 1023ull) & ~1023ull);\n";
+    k << "  unsigned long long* full = (unsigned long long*)(smem + " << A_RES + S * B_BYTES << ");\n";
+    k << "  unsigned long long* empty = full + " << S << ";\n";
+    k << "  unsigned long long* aready = empty + " << S << ";\n";
+    k << "  unsigned long long* accf = aready + 1;\n";
+    k << "  unsigned* tslot = (unsigned*)(accf + 1);\n";
+    k << "  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;\n";
+    k << "  const int tile_m = blockIdx.x * 128, tile_n = blockIdx.y * " << BN << ";\n";
+    k << "  int bzl = blockIdx.z;\n";
+    for (int b = nbC - 1; b >= 0; --b)
+      k << "  const int " << ep.batch_vars[b] << " = bzl % " << C[b] << "; bzl /= " << C[b] << ";\n";
+    k << "  (void)bzl;\n";
+    k << "  if (threadIdx.x == 0) {\n    for (int s = 0; s < " << S
+      << "; ++s) { mbar_init(full + s, 1); mbar_init(empty + s, 1); }\n"
+      << "    mbar_init(aready, 4);\n    mbar_init(accf, 1);\n    mbar_fence_init();\n    tma_prefetch(&tmB);\n  }\n";
+    k << "  if (warp == 5) tc_alloc(tslot, " << tcols << ");\n";
+    k << "  tc_fence_before();\n  __syncthreads();\n  tc_fence_after();\n";
+    k << "  const unsigned tmem = *tslot;\n";
+    k << "  pdl_trigger();\n  pdl_wait();\n";
+    k << "  if (warp < 4) {\n";
+    // prologue: one warp per A row
+    k << "    const unsigned sA = smem_u32(smem);\n    const int tid = lane;\n    const unsigned gmask = 0xffffffffu;\n"
+      << "    (void)gmask;\n";
+    k << "    #pragma unroll 1\n    for (int r = warp; r < 128; r += 4) {\n";
+    k << "      const int gm = tile_m + r;\n      if (gm >= " << M << ") break;\n";
+    k << pro.body;
+    k << "    }\n";
+    k << "    fence_async_smem();\n    __syncwarp();\n    if (lane == 0) mbar_arrive(aready);\n";
+    k << "  } else if (warp == 4 && lane == 0) {\n";
+    k << "    int s = 0; unsigned ph = 0;\n";
+    k << "    for (int kb = 0; kb < " << NKA << "; ++kb) {\n";
+    k << "      mbar_wait(empty + s, ph ^ 1u);\n";
+    k << "      mbar_expect_tx(full + s, " << B_BYTES << "u);\n";
+    k << "      unsigned char* sb = smem + " << A_RES << " + s * " << B_BYTES << ";\n";
+    if (b_kmaj) {
+      k << "      " << load << "(sb, &tmB, full + s, " << coords("kb * 64", "tile_n") << ");\n";
+    } else {
+      for (int cc = 0; cc < (BN + 63) / 64; ++cc)
+        k << "      " << load << "(sb + " << cc * 8192 << ", &tmB, full + s, " << coords("tile_n + " + str(cc * 64), "kb * 64")
+          << ");\n";
+    }
+    k << "      if (++s == " << S << ") { s = 0; ph ^= 1u; }\n    }\n";
+    k << "  } else if (warp == 5 && lane == 0) {\n";
+    k << "    mbar_wait(aready, 0);\n    tc_fence_after();\n";
+    k << "    const unsigned sa0 = smem_u32(smem);\n";
+    k << "    int s = 0; unsigned ph = 0;\n";
+    k << "    for (int kb = 0; kb < " << NKA << "; ++kb) {\n";
+    k << "      mbar_wait(full + s, ph);\n      tc_fence_after();\n";
+    k << "      const unsigned sa = sa0 + kb * 16384, sb = sa0 + " << A_RES << " + s * " << B_BYTES << ";\n";
+    k << "      #pragma unroll\n      for (int k = 0; k < 4; ++k) {\n";
+    k << "        const unsigned long long ad = umma_desc(sa + k * 32, 16, 1024);\n";
+    if (b_kmaj)
+      k << "        const unsigned long long bd = umma_desc(sb + k * 32, 16, 1024);\n";
+    else
+      k << "        const unsigned long long bd = umma_desc(sb + k * " << 16 * b_row_bytes << ", 8192, " << 8 * b_row_bytes
+        << ", " << b_swz_umma << ");\n";
+    k << "        tc_mma(tmem, ad, bd, " << idesc << "u, (kb | k) != 0);\n      }\n";
+    k << "      tc_commit(empty + s);\n";
+    k << "      if (++s == " << S << ") { s = 0; ph ^= 1u; }\n    }\n";
+    k << "    tc_commit(accf);\n  }\n";
+    k << "  __syncwarp();\n";
+    k << "  if (warp < 4) {\n    mbar_wait(accf, 0);\n    __syncwarp();\n    tc_fence_after();\n";
+    k << "    const int gm = tile_m + warp * 32 + lane;\n    const int tid = 0;\n    (void)tid;\n";
+    k << "    #pragma unroll 1\n    for (int ch = 0; ch < " << BN / CW << "; ++ch) {\n";
+    k << "      const int nb = tile_n + ch * " << CW << ";\n";
+    k << "      float acc[" << CW << "];\n";
+    k << "      tc_ld" << CW << "(tmem + ((unsigned)(warp * 32) << 16) + (unsigned)(ch * " << CW << "), acc);\n";
+    k << "      if (gm < " << M << " && nb < " << N << ") {\n";
+    k << ep.body << ep.store;
+    k << "      }\n    }\n  }\n";
+    k << "  tc_fence_before();\n  __syncthreads();\n";
+    k << "  if (warp == 5) tc_dealloc(tmem, " << tcols << ");\n}\n";
+    KernelVariant kv;
+    std::string src = k.str();
+    char nm[64];
+    std::snprintf(nm, sizeof nm, "korch_pgemm_%016llx", (unsigned long long)fnv1a(std::string(kSm100GemmTemplate) + "\n" + src));
+    kv.name = nm;
+    src.replace(src.find("KNAME"), 5, kv.name);
+    kv.source = src;
+    kv.tcgen05 = true;
+    kv.block = 192;
+    kv.grid = Mt;
+    kv.grid_y = Nt;
+    kv.grid_z = batch;
+    kv.smem = smem;
+    kv.tma = {db};
+    std::ostringstream t;
+    t << "gemm-prologue BM=128 BN=" << BN << " K=" << K << " stagesB=" << S << " B=" << (b_kmaj ? "K" : "N")
+      << "-major M=" << M << " N=" << N << " batch=" << batch;
+    kv.tag = t.str();
+    kp.ext = ep.ext;
+    kp.bytes = ep.bytes + pro.bytes + 2 * numel(vb.shape);
+    kp.variants.push_back(kv);
+  }
+  if (!kp.variants.empty()) {
+    kp.klass = KORCH_CLASS_GEMM;
+    kp.reject.clear();
+  }
+  return kp;
+}
+
 KernelPlan generate_gemm(const Graph& g, const Candidate& c) {
   KernelPlan kp;
   kp.klass = KORCH_CLASS_REJECTED;
@@ -370,6 +568,14 @@ KernelPlan generate_gemm(const Graph& g, const Candidate& c) {
   View va, vb;
   std::set<int> chain;
   std::string err;
+  {
+    // A computed in the kernel (not a view of an external tensor): the prologue GEMM
+    View t;
+    std::set<int> ch;
+    std::string e2;
+    const Ref& a = L.in[0];
+    if (!a.is_input && mem.count(a.id) && !operand_view(g, mem, L, 0, &t, &ch, &e2)) return generate_prologue_gemm(g, c, mm);
+  }
   if (!operand_view(g, mem, L, 0, &va, &chain, &err) || !operand_view(g, mem, L, 1, &vb, &chain, &err)) {
     kp.reject = err;
     return kp;

@@ -272,6 +272,31 @@ def test_long_elementwise_rows_chunked(ctx, dtype):
     _every_variant(c, gen, exact=False)
 
 
+def _ln_linear_graph(m, k, n, batch=1):
+    b = GraphBuilder("bf16")
+    x = b.input("x", [batch, m, k])
+    g = b.input("g", [k], mean=1.0, std=0.1)
+    be = b.input("be", [k], std=0.1)
+    w = b.input("w", [k, n], std=k ** -0.5)
+    bias = b.input("bias", [n], std=0.1)
+    y = b.op("LayerNorm", x, g, be, axis=-1, eps=1e-5)
+    y = b.op("MatMul", y, w)
+    y = b.op("Add", y, bias)
+    b.output(b.op("GELU", y))
+    return b.build()
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("m,k,n,batch", [(128, 768, 256, 1), (200, 256, 48, 1), (70, 64, 200, 2)])
+def test_prologue_gemm_every_variant(ctx, m, k, n, batch):
+    """KB5-P: LayerNorm computed in the GEMM's A prologue (resident swizzled A tile),
+    ragged M and N, batched, every launch variant."""
+    c = Case(ctx, _ln_linear_graph(m, k, n, batch))
+    idx = [x["index"] for x in c.cands if "prologue" in _tags(c, x["index"])]
+    assert any(len(c.cands[i]["members"]) >= 12 for i in idx)
+    _every_variant(c, idx, exact=False)
+
+
 def _tags(c, i):
     nv, ch, _ = c.kg.variant_info(i)
     t = []
