@@ -71,6 +71,7 @@ struct GemmPrologue {
   std::string body;
   int64_t bytes = 0;                  // prologue reads (the A tile never reaches HBM)
   std::vector<std::string> batch_vars;
+  int stage_slot = -1;                // ext slot of the tensor TMA-loaded into the A tile (-1: none)
 };
 bool make_gemm_prologue(const Graph& g, const Candidate& c, int mm, const std::vector<Ref>& pre_ext,
                         GemmPrologue* out, std::string* err);

@@ -409,7 +409,7 @@ static KernelPlan generate_prologue_gemm(const Graph& g, const Candidate& c, int
     const int budget = 227 * 1024 - A_RES - 1024 - 256;
     const int S = (int)std::min<int64_t>(NKA, budget / B_BYTES);
     if (S < 2) { kp.reject = "prologue GEMM: shared memory"; continue; }
-    const int smem = A_RES + S * B_BYTES + 1024 + (2 * S + 2) * 8 + 16;
+    const int smem = A_RES + S * B_BYTES + 1024 + (2 * S + 3) * 8 + 16;
     const int tcols = BN < 32 ? 32 : BN;
     const int64_t Mt = (M + 127) / 128, Nt = (N + BN - 1) / BN;
     const int bmn_box = BN < 64 ? BN : 64;
@@ -439,6 +439,33 @@ static KernelPlan generate_prologue_gemm(const Graph& g, const Candidate& c, int
         if (db.strides[i] % 16 || db.strides[i] <= 0) ok = false;
       if (!ok) { kp.reject = "prologue GEMM: B strides not TMA-able"; continue; }
     }
+    // the A-shaped external operand (e.g. the LayerNorm input) arrives by TMA in the
+    // resident A tile's own swizzled layout; the prologue then transforms it in place
+    const bool staged = pro.stage_slot >= 0;
+    TmaDesc dx;
+    std::vector<int> bx_axes;
+    if (staged) {
+      dx.tensor = pro.stage_slot;
+      dx.dtype = 1;
+      dx.swizzle = 3;
+      dx.elem_off = 0;
+      dx.rank = 0;
+      auto push = [&](int64_t dim, int64_t st, uint32_t box) {
+        dx.dims[dx.rank] = dim; dx.strides[dx.rank] = st * 2; dx.box[dx.rank] = box; dx.rank++;
+      };
+      push(K, 1, 64);
+      push(M, K, 128);
+      int64_t st = M * K;
+      for (int b = nbC - 1; b >= 0; --b) {
+        if (as[b] > 1) {
+          if (dx.rank >= 5) { kp.reject = "prologue GEMM: staged operand rank"; break; }
+          push(as[b], st, 1);
+          bx_axes.push_back(b);
+        }
+        st *= as[b];
+      }
+      if (dx.rank > 5 || (dx.rank == 5 && bx_axes.size() + 2 != 5)) continue;
+    }
     const uint32_t idesc = (1u << 4) | (1u << 7) | (1u << 10) | ((b_kmaj ? 0u : 1u) << 16) |
                            ((uint32_t)(BN >> 3) << 17) | ((uint32_t)(128 >> 4) << 24);
     auto coords = [&](const std::string& inner, const std::string& outer) {
@@ -452,7 +479,7 @@ static KernelPlan generate_prologue_gemm(const Graph& g, const Candidate& c, int
     for (size_t i = 0; i < ep.ext.size(); ++i)
       k << "const " << (g.dtype_of(ep.ext[i]) == DType::F32 ? "float" : "bf16_t") << "* __restrict__ p" << i << ", ";
     k << (g.prims[c.output].dtype == DType::F32 ? "float" : "bf16_t") << "* __restrict__ out, "
-      << "const __grid_constant__ TmaMap tmB) {\n";
+      << "const __grid_constant__ TmaMap tmB" << (staged ? ", const __grid_constant__ TmaMap tmX" : "") << ") {\n";
     k << "  typedef " << (numel(C) >= (1LL << 31) ? "long long" : "int") << " idx_t;\n";
     k << "  extern __shared__ __align__(1024) unsigned char smem_raw[];\n";
     k << "  unsigned char* smem = (unsigned char*)(((unsigned long long)smem_raw + 1023ull) & ~1023ull);\n";
@@ -460,7 +487,8 @@ static KernelPlan generate_prologue_gemm(const Graph& g, const Candidate& c, int
     k << "  unsigned long long* empty = full + " << S << ";\n";
     k << "  unsigned long long* aready = empty + " << S << ";\n";
     k << "  unsigned long long* accf = aready + 1;\n";
-    k << "  unsigned* tslot = (unsigned*)(accf + 1);\n";
+    k << "  unsigned long long* xfull = accf + 1;\n";
+    k << "  unsigned* tslot = (unsigned*)(xfull + 1);\n";
     k << "  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;\n";
     k << "  const int tile_m = blockIdx.x * 128, tile_n = blockIdx.y * " << BN << ";\n";
     k << "  int bzl = blockIdx.z;\n";
@@ -469,7 +497,8 @@ static KernelPlan generate_prologue_gemm(const Graph& g, const Candidate& c, int
     k << "  (void)bzl;\n";
     k << "  if (threadIdx.x == 0) {\n    for (int s = 0; s < " << S
       << "; ++s) { mbar_init(full + s, 1); mbar_init(empty + s, 1); }\n"
-      << "    mbar_init(aready, 4);\n    mbar_init(accf, 1);\n    mbar_fence_init();\n    tma_prefetch(&tmB);\n  }\n";
+      << "    mbar_init(aready, 4);\n    mbar_init(accf, 1);\n    mbar_init(xfull, 1);\n    mbar_fence_init();\n"
+      << "    tma_prefetch(&tmB);\n" << (staged ? "    tma_prefetch(&tmX);\n" : "") << "  }\n";
     k << "  if (warp == 5) tc_alloc(tslot, " << tcols << ");\n";
     k << "  tc_fence_before();\n  __syncthreads();\n  tc_fence_after();\n";
     k << "  const unsigned tmem = *tslot;\n";
@@ -478,12 +507,20 @@ static KernelPlan generate_prologue_gemm(const Graph& g, const Candidate& c, int
     // prologue: one warp per A row
     k << "    const unsigned sA = smem_u32(smem);\n    const int tid = lane;\n    const unsigned gmask = 0xffffffffu;\n"
       << "    (void)gmask;\n";
+    if (staged) k << "    mbar_wait(xfull, 0);\n";
     k << "    #pragma unroll 1\n    for (int r = warp; r < 128; r += 4) {\n";
     k << "      const int gm = tile_m + r;\n      if (gm >= " << M << ") break;\n";
     k << pro.body;
     k << "    }\n";
     k << "    fence_async_smem();\n    __syncwarp();\n    if (lane == 0) mbar_arrive(aready);\n";
     k << "  } else if (warp == 4 && lane == 0) {\n";
+    if (staged) {
+      std::string xc;
+      for (int b : bx_axes) xc += ", " + ep.batch_vars[b];
+      k << "    mbar_expect_tx(xfull, " << A_RES << "u);\n";
+      k << "    for (int kb = 0; kb < " << NKA << "; ++kb)\n";
+      k << "      tma_load_" << dx.rank << "d(smem + kb * 16384, &tmX, xfull, kb * 64, tile_m" << xc << ");\n";
+    }
     k << "    int s = 0; unsigned ph = 0;\n";
     k << "    for (int kb = 0; kb < " << NKA << "; ++kb) {\n";
     k << "      mbar_wait(empty + s, ph ^ 1u);\n";
@@ -541,8 +578,9 @@ static KernelPlan generate_prologue_gemm(const Graph& g, const Candidate& c, int
     kv.grid_z = batch;
     kv.smem = smem;
     kv.tma = {db};
+    if (staged) kv.tma.push_back(dx);
     std::ostringstream t;
-    t << "gemm-prologue BM=128 BN=" << BN << " K=" << K << " stagesB=" << S << " B=" << (b_kmaj ? "K" : "N")
+    t << "gemm-prologue" << (staged ? "-tma" : "") << " BM=128 BN=" << BN << " K=" << K << " stagesB=" << S << " B=" << (b_kmaj ? "K" : "N")
       << "-major M=" << M << " N=" << N << " batch=" << batch;
     kv.tag = t.str();
     kp.ext = ep.ext;

@@ -35,6 +35,15 @@ static __device__ __forceinline__ void fence_async_smem() {
 static __device__ __forceinline__ void st_shared_v4(unsigned addr, uint4 v) {
   asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(addr), "r"(v.x), "r"(v.y), "r"(v.z), "r"(v.w) : "memory");
 }
+// 8 bf16 from shared memory (one 16-byte swizzle chunk) -> 8 floats
+static __device__ __forceinline__ void ld_shared_bf16x8(unsigned addr, float* v) {
+  unsigned a, b, c, d;
+  asm volatile("ld.shared.v4.b32 {%0, %1, %2, %3}, [%4];" : "=r"(a), "=r"(b), "=r"(c), "=r"(d) : "r"(addr) : "memory");
+  v[0] = __uint_as_float(a << 16); v[1] = __uint_as_float(a & 0xffff0000u);
+  v[2] = __uint_as_float(b << 16); v[3] = __uint_as_float(b & 0xffff0000u);
+  v[4] = __uint_as_float(c << 16); v[5] = __uint_as_float(c & 0xffff0000u);
+  v[6] = __uint_as_float(d << 16); v[7] = __uint_as_float(d & 0xffff0000u);
+}
 static __device__ __forceinline__ void mbar_wait(unsigned long long* b, unsigned parity) {
   asm volatile(
       "{\n"
