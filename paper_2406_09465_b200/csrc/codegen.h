@@ -57,11 +57,14 @@ struct GemmEpilogue {
   std::string body, store;
   int64_t bytes = 0;                  // epilogue reads + output write
   std::vector<std::string> batch_vars;
+  bool rows_unit = false;             // output address has unit stride along the row gm
 };
+// t > 1: t threads share each row chunk (column-lane epilogue, see gemm_gen.cpp); the
+// body then reads float acc[cw / t] for columns nb + (tid + k*t)*8 + [0, 8).
 // target >= 0: compute that intermediate node instead of the candidate's output; then
 // `store` holds the name of the float[cw] array with its values (no global store).
 bool make_gemm_epilogue(const Graph& g, const Candidate& c, int mm, int cw, const std::vector<Ref>& pre_ext,
-                        GemmEpilogue* out, std::string* err, int target = -1);
+                        GemmEpilogue* out, std::string* err, int target = -1, int t = 1);
 // Prologue of a GEMM whose A operand is computed in the kernel (e.g. LayerNorm feeding a
 // Linear): `body` runs once per A row (local row r, global row gm; one warp per row,
 // lane = tid) and writes the bf16 row into the resident, 128B-swizzled K-major A tile at

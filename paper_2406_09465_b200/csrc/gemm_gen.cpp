@@ -27,6 +27,11 @@ struct View {
   std::vector<int64_t> coef;    // per operand axis (batch..., row, col), elements
   int64_t off = 0;              // element offset
   Shape shape;                  // operand shape
+  // K-split view: the contraction axis k addresses (k % ksplit) * coef[k axis] +
+  // (k / ksplit) * kout, e.g. the head-merge Transpose+Reshape in front of an attention
+  // output projection (A[s, h*64 + d] = O[h, s, d]).  A 64-wide K-block never straddles
+  // a split when ksplit % 64 == 0, so TMA loads it as one box of a rank+1 tensor map.
+  int64_t ksplit = 0, kout = 0;
 };
 
 bool operand_view(const Graph& g, const std::set<int>& mem, const Prim& L, int slot, View* v, std::set<int>* chain,
@@ -79,19 +84,36 @@ bool operand_view(const Graph& g, const std::set<int>& mem, const Prim& L, int s
     addr = ExprCtx::add(addr, ExprCtx::scale(co[k], st));
     st *= ts[k];
   }
-  for (auto& t : addr.terms)
-    if (t.second.type != Atom::Var) {
+  // the contraction axis: A = [.., M, K] (last), B = [.., K, N] (second to last)
+  const int kax = slot == 0 ? (int)s.size() - 1 : (int)s.size() - 2;
+  int64_t D = 0, cdiv = 0, cmod = 0;
+  for (auto& t : addr.terms) {
+    const Atom& at = t.second;
+    if (at.type == Atom::Var) continue;
+    const bool on_k = (at.type == Atom::Div || at.type == Atom::Mod) && at.sub && at.sub->c0 == 0 &&
+                      at.sub->terms.size() == 1 && at.sub->terms[0].first == 1 &&
+                      at.sub->terms[0].second.type == Atom::Var && at.sub->terms[0].second.var == vars[kax];
+    if (!on_k || (D && at.c != D) || s[kax] % at.c) {
       *err = "operand view is not affine (layout chain does not fold into strides)";
       return false;
     }
+    D = at.c;
+    (at.type == Atom::Div ? cdiv : cmod) += t.first;
+  }
   v->src = r;
   v->shape = s;
   v->off = addr.c0;
   v->coef.assign(s.size(), 0);
   for (size_t i = 0; i < s.size(); ++i) {
     int64_t c = 0;
-    ExprCtx::linear_in(addr, vars[i], &c);
+    for (auto& t : addr.terms)
+      if (t.second.type == Atom::Var && t.second.var == vars[i]) c += t.first;
     v->coef[i] = c;
+  }
+  if (D) {  // k = D * (k / D) + k % D
+    v->ksplit = D;
+    v->kout = cdiv + v->coef[kax] * D;
+    v->coef[kax] += cmod;
   }
   return true;
 }
@@ -119,6 +141,92 @@ struct GatherSpec {
   std::string prefix;             // kernel name prefix
   int64_t b_bytes = 0;            // algorithmic bytes of B
 };
+
+
+// Fused epilogue over a 128 x BN TMEM accumulator tile.  Warp w (< 4) owns TMEM lanes
+// 32w..32w+31 = tile rows tile_m + 32w + lane; `ep` was emitted with
+// make_gemm_epilogue(cw = CW, t = T).
+//  * T == 1 (row mapping): each thread runs the epilogue on its own row, CW columns per
+//    pass; coalesced when the output is contiguous along rows (ep.rows_unit).
+//  * T > 1 (column-lane mapping): each CW-column chunk goes TMEM -> registers -> the warp's
+//    slice of a shared staging buffer (pitch CW + 4 floats, conflict-free 16-byte writes
+//    and reads) and is re-read with T lanes per row, so one warp instruction of the side
+//    reads and of the store covers 32/T rows of 8T contiguous columns instead of 32 rows
+//    of 16 bytes.  The staging buffer aliases the operand ring, which is idle once the
+//    accumulator barrier has fired (every TMA load was consumed by an MMA before it).
+static int stage_pitch(int CW) { return CW + 4; }
+static int stage_bytes(int CW) { return 4 * 32 * stage_pitch(CW) * 4; }
+
+static std::string emit_tmem_epilogue(const GemmEpilogue& ep, int BN, int CW, int T, int64_t M, int64_t N,
+                                      const std::string& tmem = "tmem") {
+  std::ostringstream k;
+  auto tmem_load = [&](const char* dst) {
+    std::ostringstream t;
+    if (CW <= 32) {
+      t << "      tc_ld" << CW << "(" << tmem << " + ((unsigned)(warp * 32) << 16) + (unsigned)(ch * " << CW << "), " << dst
+        << ");\n";
+    } else {
+      t << "      #pragma unroll\n      for (int q = 0; q < " << CW / 32 << "; ++q)\n"
+        << "        tc_ld32(" << tmem << " + ((unsigned)(warp * 32) << 16) + (unsigned)(ch * " << CW << " + q * 32), " << dst
+        << " + q * 32);\n";
+    }
+    return t.str();
+  };
+  if (T == 1) {
+    k << "  {\n    const int gm = tile_m + warp * 32 + lane;\n    const int tid = 0;\n    (void)tid;\n";
+    k << "    #pragma unroll 1\n    for (int ch = 0; ch < " << BN / CW << "; ++ch) {\n";
+    k << "      const int nb = tile_n + ch * " << CW << ";\n";
+    k << "      float acc[" << CW << "];\n";
+    k << tmem_load("acc");
+    k << "      if (gm < " << M << " && nb < " << N << ") {\n";
+    k << ep.body << ep.store;
+    k << "      }\n    }\n  }\n";
+    return k.str();
+  }
+  const int P = stage_pitch(CW), R = 32 / T;
+  k << "  {\n    float* stg = reinterpret_cast<float*>(smem) + warp * " << 32 * P << ";\n";
+  k << "    const int tid = lane % " << T << ", rsub = lane / " << T << ";\n";
+  k << "    #pragma unroll 1\n    for (int ch = 0; ch < " << BN / CW << "; ++ch) {\n";
+  k << "      const int nb = tile_n + ch * " << CW << ";\n";
+  k << "      if (nb >= " << N << ") break;  // chunk wholly past N (uniform)\n";
+  k << "      {\n        float accr[" << CW << "];\n";
+  k << tmem_load("accr");
+  k << "        #pragma unroll\n        for (int q = 0; q < " << CW / 4 << "; ++q)\n";
+  k << "          *reinterpret_cast<float4*>(stg + lane * " << P << " + 4 * q) = "
+       "make_float4(accr[4 * q], accr[4 * q + 1], accr[4 * q + 2], accr[4 * q + 3]);\n      }\n";
+  k << "      __syncwarp();\n";
+  // Rows past M (ragged last tile) compute on a clamped row and skip the store, so every
+  // pass's side reads are unconditional and the unrolled passes keep their loads in
+  // flight together (columns past N: whole chunks are skipped above, a partial chunk is
+  // masked inside the body, N % CW != 0).
+  k << "      #pragma unroll\n      for (int pp = 0; pp < " << T << "; ++pp) {\n";
+  k << "        const int rl = pp * " << R << " + rsub;\n";
+  k << "        const int gmr = tile_m + warp * 32 + rl;\n";
+  k << "        const int gm = gmr < " << M << " ? gmr : " << M - 1 << ";\n";
+  k << "        float acc[8];\n";
+  k << "        {\n          const float4 a0 = *reinterpret_cast<const float4*>(stg + rl * " << P << " + tid * 8);\n";
+  k << "          const float4 a1 = *reinterpret_cast<const float4*>(stg + rl * " << P << " + tid * 8 + 4);\n";
+  k << "          acc[0] = a0.x; acc[1] = a0.y; acc[2] = a0.z; acc[3] = a0.w;\n";
+  k << "          acc[4] = a1.x; acc[5] = a1.y; acc[6] = a1.z; acc[7] = a1.w;\n        }\n";
+  k << "        {\n" << ep.body << "        if (gmr < " << M << ") {\n" << ep.store << "        }\n        }\n";
+  k << "      }\n      __syncwarp();\n    }\n  }\n";
+  return k.str();
+}
+
+// Column-lane epilogue choice: T = CW / 8 lanes per row unless the output is contiguous
+// along rows (then the row mapping already stores coalesced) or the epilogue reduces rows.
+static int epilogue_lanes(const Graph& g, const Candidate& c, int mm, int CW, const std::vector<Ref>& pre,
+                          int64_t ring_bytes, GemmEpilogue* ep) {
+  if (ep->rows_unit || CW % 8 || CW > 32 || stage_bytes(CW) > ring_bytes) return 1;
+  for (int m : c.members)
+    if (g.prims[m].kind == Kind::Reduce) return 1;
+  GemmEpilogue e2;
+  std::string err;
+  if (!make_gemm_epilogue(g, c, mm, CW, pre, &e2, &err, -1, CW / 8)) return 1;
+  if (e2.ext.size() != ep->ext.size()) return 1;
+  *ep = e2;
+  return CW / 8;
+}
 
 static KernelPlan generate_gather_gemm(const Graph& g, const Candidate& c, int mm, const GatherSpec& gs);
 
@@ -186,6 +294,7 @@ static KernelPlan generate_matmul_gather(const Graph& g, const Candidate& c, int
     if (C[i] != 1) { kp.reject = "gather GEMM: batched"; return kp; }
   const int nbA = (int)va.shape.size() - 2, nbB = (int)vb.shape.size() - 2;
   const int64_t M = C[C.size() - 2], N = C.back(), K = va.shape.back();
+  if (va.ksplit || vb.ksplit) { kp.reject = "gather GEMM: K-split view"; return kp; }
   if (va.coef[nbA + 1] != 1 || (va.off * 2) % 16 || (va.coef[nbA] * 2) % 16 || va.coef[nbA] <= 0 || K % 8) {
     kp.reject = "gather GEMM: A not a 16-byte aligned K-major view";
     return kp;
@@ -235,6 +344,7 @@ static KernelPlan generate_gather_gemm(const Graph& g, const Candidate& c, int m
     const int A_BYTES = 128 * 64 * 2, B_BYTES = BN * 64 * 2, STAGE = A_BYTES + B_BYTES;
     const int S_ = (int)std::max<int64_t>(2, std::min<int64_t>({NK, 4, (200 * 1024) / STAGE}));
     const int smem = S_ * STAGE + 1024 + (2 * S_ + 1) * 8 + 16;
+    const int TE = epilogue_lanes(g, c, mm, 32, pre, (int64_t)S_ * STAGE, &ep);
     const int64_t Nt = (NP + BN - 1) / BN;
     const int tcols = BN;
     const uint32_t idesc = (1u << 4) | (1u << 7) | (1u << 10) | (0u << 15) | (1u << 16) |
@@ -264,7 +374,15 @@ static KernelPlan generate_gather_gemm(const Graph& g, const Candidate& c, int m
     k << "  const int tile_m = blockIdx.x * 128, tile_n = blockIdx.y * " << BN << ";\n";
     k << "  if (threadIdx.x == 0) {\n    for (int s = 0; s < " << S_
       << "; ++s) { mbar_init(full + s, 5); mbar_init(empty + s, 1); }\n"
-      << "    mbar_init(accf, 1);\n    mbar_fence_init();\n    tma_prefetch(&tmA);\n  }\n";
+      << "    mbar_init(accf, 1);\n    mbar_fence_init();\n    tma_prefetch(&tmA);\n";
+    // weights (a graph input): first PRE stages fetched before the programmatic-dependency wait
+    const int64_t PRE = gs.a_src.is_input ? std::min<int64_t>(S_, NK) : 0;
+    if (PRE) {
+      k << "    for (int s = 0; s < " << PRE << "; ++s) {\n";
+      k << "      mbar_expect_tx(full + s, " << A_BYTES << "u);\n";
+      k << "      tma_load_2d(smem + s * " << STAGE << ", &tmA, full + s, s * 64, tile_m);\n    }\n";
+    }
+    k << "  }\n";
     k << "  if (warp == 5) tc_alloc(tslot, " << tcols << ");\n";
     k << "  tc_fence_before();\n  __syncthreads();\n  tc_fence_after();\n";
     k << "  const unsigned tmem = *tslot;\n";
@@ -300,8 +418,9 @@ static KernelPlan generate_gather_gemm(const Graph& g, const Candidate& c, int m
     k << "    int s = 0; unsigned ph = 0;\n";
     k << "    for (int kb = 0; kb < " << NK << "; ++kb) {\n";
     k << "      mbar_wait(empty + s, ph ^ 1u);\n";
+    k << "      if (kb >= " << PRE << ") {\n";
     k << "      mbar_expect_tx(full + s, " << A_BYTES << "u);\n";
-    k << "      tma_load_2d(smem + s * " << STAGE << ", &tmA, full + s, kb * 64, tile_m);\n";
+    k << "      tma_load_2d(smem + s * " << STAGE << ", &tmA, full + s, kb * 64, tile_m);\n      }\n";
     k << "      if (++s == " << S_ << ") { s = 0; ph ^= 1u; }\n    }\n";
     // MMA: warp 5
     k << "  } else if (warp == 5 && lane == 0) {\n";
@@ -319,14 +438,8 @@ static KernelPlan generate_gather_gemm(const Graph& g, const Candidate& c, int m
     // epilogue: warps 0-3 (TMEM lane quarters 0-3)
     k << "  __syncwarp();\n";
     k << "  if (warp < 4) {\n    mbar_wait(accf, 0);\n    __syncwarp();\n    tc_fence_after();\n";
-    k << "    const int gm = tile_m + warp * 32 + lane;\n    const int tid = 0;\n    (void)tid;\n";
-    k << "    #pragma unroll 1\n    for (int ch = 0; ch < " << BN / 32 << "; ++ch) {\n";
-    k << "      const int nb = tile_n + ch * 32;\n";
-    k << "      float acc[32];\n";
-    k << "      tc_ld32(tmem + ((unsigned)(warp * 32) << 16) + (unsigned)(ch * 32), acc);\n";
-    k << "      if (gm < " << F << " && nb < " << NP << ") {\n";
-    k << ep.body << ep.store;
-    k << "      }\n    }\n  }\n";
+    k << emit_tmem_epilogue(ep, BN, 32, TE, F, NP);
+    k << "  }\n";
     k << "  tc_fence_before();\n  __syncthreads();\n";
     k << "  if (warp == 5) tc_dealloc(tmem, " << tcols << ");\n}\n";
 
@@ -347,7 +460,7 @@ static KernelPlan generate_gather_gemm(const Graph& g, const Candidate& c, int m
     kv.smem = smem;
     kv.tma = {da};
     std::ostringstream t;
-    t << gs.tag << " BM=128 BN=" << BN << " BK=64 stages=" << S_;
+    t << gs.tag << " BM=128 BN=" << BN << " BK=64 stages=" << S_ << (TE > 1 ? " epi=cl" : "");
     kv.tag = t.str();
     kp.variants.push_back(kv);
   }
@@ -376,6 +489,7 @@ static KernelPlan generate_prologue_gemm(const Graph& g, const Candidate& c, int
   std::string err;
   if (L.kind != Kind::MatMul) { kp.reject = "prologue GEMM: MatMul only"; return kp; }
   if (!operand_view(g, mem, L, 1, &vb, &chainB, &err)) { kp.reject = "prologue GEMM B: " + err; return kp; }
+  if (vb.ksplit) { kp.reject = "prologue GEMM B: K-split view"; return kp; }
   if (g.dtype_of(vb.src) != DType::BF16) { kp.reject = "prologue GEMM: B must be bf16"; return kp; }
   for (int m : c.members)
     if (g.prims[m].kind == Kind::Reduce && g.topo_index[m] > g.topo_index[mm]) {
@@ -408,8 +522,9 @@ static KernelPlan generate_prologue_gemm(const Graph& g, const Candidate& c, int
     const int B_BYTES = BN * 64 * 2;
     const int budget = 227 * 1024 - A_RES - 1024 - 256;
     const int S = (int)std::min<int64_t>(NKA, budget / B_BYTES);
-    if (S < 2) { kp.reject = "prologue GEMM: shared memory"; continue; }
+    if (S < std::min<int64_t>(2, NKA)) { kp.reject = "prologue GEMM: shared memory"; continue; }
     const int smem = A_RES + S * B_BYTES + 1024 + (2 * S + 3) * 8 + 16;
+    const int TE = epilogue_lanes(g, c, mm, CW, pro.ext, (int64_t)A_RES + (int64_t)S * B_BYTES, &ep);
     const int tcols = BN < 32 ? 32 : BN;
     const int64_t Mt = (M + 127) / 128, Nt = (N + BN - 1) / BN;
     const int bmn_box = BN < 64 ? BN : 64;
@@ -495,10 +610,40 @@ static KernelPlan generate_prologue_gemm(const Graph& g, const Candidate& c, int
     for (int b = nbC - 1; b >= 0; --b)
       k << "  const int " << ep.batch_vars[b] << " = bzl % " << C[b] << "; bzl /= " << C[b] << ";\n";
     k << "  (void)bzl;\n";
+    // B loads (kb, sb, s in scope)
+    std::ostringstream ldb;
+    if (b_kmaj) {
+      ldb << "      " << load << "(sb, &tmB, full + s, " << coords("kb * 64", "tile_n") << ");\n";
+    } else {
+      for (int cc = 0; cc < (BN + 63) / 64; ++cc)
+        ldb << "      " << load << "(sb + " << cc * 8192 << ", &tmB, full + s, " << coords("tile_n + " + str(cc * 64), "kb * 64")
+            << ");\n";
+    }
+    std::string xc;
+    for (int b : bx_axes) xc += ", " + ep.batch_vars[b];
+    std::ostringstream ldx;
+    if (staged) {
+      ldx << "    mbar_expect_tx(xfull, " << A_RES << "u);\n";
+      ldx << "    for (int kb = 0; kb < " << NKA << "; ++kb)\n";
+      ldx << "      tma_load_" << dx.rank << "d(smem + kb * 16384, &tmX, xfull, kb * 64, tile_m" << xc << ");\n";
+    }
+    // graph-input operands (weights; the staged LayerNorm input when it is a graph input)
+    // are fetched right after barrier init, before the programmatic-dependency wait
+    const bool earlyB = vb.src.is_input;
+    const bool earlyX = staged && pro.ext[pro.stage_slot].is_input;
+    const int64_t PRE = earlyB ? std::min<int64_t>(S, NKA) : 0;
     k << "  if (threadIdx.x == 0) {\n    for (int s = 0; s < " << S
       << "; ++s) { mbar_init(full + s, 1); mbar_init(empty + s, 1); }\n"
       << "    mbar_init(aready, 4);\n    mbar_init(accf, 1);\n    mbar_init(xfull, 1);\n    mbar_fence_init();\n"
-      << "    tma_prefetch(&tmB);\n" << (staged ? "    tma_prefetch(&tmX);\n" : "") << "  }\n";
+      << "    tma_prefetch(&tmB);\n" << (staged ? "    tma_prefetch(&tmX);\n" : "");
+    if (earlyX) k << ldx.str();
+    if (PRE) {
+      k << "    for (int s = 0; s < " << PRE << "; ++s) {\n      const int kb = s;\n";
+      k << "      mbar_expect_tx(full + s, " << B_BYTES << "u);\n";
+      k << "      unsigned char* sb = smem + " << A_RES << " + s * " << B_BYTES << ";\n";
+      k << ldb.str() << "    }\n";
+    }
+    k << "  }\n";
     k << "  if (warp == 5) tc_alloc(tslot, " << tcols << ");\n";
     k << "  tc_fence_before();\n  __syncthreads();\n  tc_fence_after();\n";
     k << "  const unsigned tmem = *tslot;\n";
@@ -514,25 +659,14 @@ static KernelPlan generate_prologue_gemm(const Graph& g, const Candidate& c, int
     k << "    }\n";
     k << "    fence_async_smem();\n    __syncwarp();\n    if (lane == 0) mbar_arrive(aready);\n";
     k << "  } else if (warp == 4 && lane == 0) {\n";
-    if (staged) {
-      std::string xc;
-      for (int b : bx_axes) xc += ", " + ep.batch_vars[b];
-      k << "    mbar_expect_tx(xfull, " << A_RES << "u);\n";
-      k << "    for (int kb = 0; kb < " << NKA << "; ++kb)\n";
-      k << "      tma_load_" << dx.rank << "d(smem + kb * 16384, &tmX, xfull, kb * 64, tile_m" << xc << ");\n";
-    }
+    if (staged && !earlyX) k << ldx.str();
     k << "    int s = 0; unsigned ph = 0;\n";
     k << "    for (int kb = 0; kb < " << NKA << "; ++kb) {\n";
     k << "      mbar_wait(empty + s, ph ^ 1u);\n";
+    k << "      if (kb >= " << PRE << ") {\n";
     k << "      mbar_expect_tx(full + s, " << B_BYTES << "u);\n";
     k << "      unsigned char* sb = smem + " << A_RES << " + s * " << B_BYTES << ";\n";
-    if (b_kmaj) {
-      k << "      " << load << "(sb, &tmB, full + s, " << coords("kb * 64", "tile_n") << ");\n";
-    } else {
-      for (int cc = 0; cc < (BN + 63) / 64; ++cc)
-        k << "      " << load << "(sb + " << cc * 8192 << ", &tmB, full + s, " << coords("tile_n + " + str(cc * 64), "kb * 64")
-          << ");\n";
-    }
+    k << ldb.str() << "      }\n";
     k << "      if (++s == " << S << ") { s = 0; ph ^= 1u; }\n    }\n";
     k << "  } else if (warp == 5 && lane == 0) {\n";
     k << "    mbar_wait(aready, 0);\n    tc_fence_after();\n";
@@ -554,14 +688,8 @@ static KernelPlan generate_prologue_gemm(const Graph& g, const Candidate& c, int
     k << "    tc_commit(accf);\n  }\n";
     k << "  __syncwarp();\n";
     k << "  if (warp < 4) {\n    mbar_wait(accf, 0);\n    __syncwarp();\n    tc_fence_after();\n";
-    k << "    const int gm = tile_m + warp * 32 + lane;\n    const int tid = 0;\n    (void)tid;\n";
-    k << "    #pragma unroll 1\n    for (int ch = 0; ch < " << BN / CW << "; ++ch) {\n";
-    k << "      const int nb = tile_n + ch * " << CW << ";\n";
-    k << "      float acc[" << CW << "];\n";
-    k << "      tc_ld" << CW << "(tmem + ((unsigned)(warp * 32) << 16) + (unsigned)(ch * " << CW << "), acc);\n";
-    k << "      if (gm < " << M << " && nb < " << N << ") {\n";
-    k << ep.body << ep.store;
-    k << "      }\n    }\n  }\n";
+    k << emit_tmem_epilogue(ep, BN, CW, TE, M, N);
+    k << "  }\n";
     k << "  tc_fence_before();\n  __syncthreads();\n";
     k << "  if (warp == 5) tc_dealloc(tmem, " << tcols << ");\n}\n";
     KernelVariant kv;
@@ -581,7 +709,7 @@ static KernelPlan generate_prologue_gemm(const Graph& g, const Candidate& c, int
     if (staged) kv.tma.push_back(dx);
     std::ostringstream t;
     t << "gemm-prologue" << (staged ? "-tma" : "") << " BM=128 BN=" << BN << " K=" << K << " stagesB=" << S << " B=" << (b_kmaj ? "K" : "N")
-      << "-major M=" << M << " N=" << N << " batch=" << batch;
+      << "-major M=" << M << " N=" << N << " batch=" << batch << (TE > 1 ? " epi=cl" : "");
     kv.tag = t.str();
     kp.ext = ep.ext;
     kp.bytes = ep.bytes + pro.bytes + 2 * numel(vb.shape);
@@ -661,6 +789,10 @@ KernelPlan generate_gemm(const Graph& g, const Candidate& c) {
     kp.reject = "operand view offset not 16-byte aligned";
     return kp;
   }
+  if ((va.ksplit && (va.ksplit % 64 || !a_kmaj || K == 1)) || (vb.ksplit && (vb.ksplit % 64 || K == 1))) {
+    kp.reject = "K-split operand view needs 64-aligned splits (and a K-major A)";
+    return kp;
+  }
 
   auto build_desc = [&](const View& v, int ext_idx, int64_t inner_dim, int64_t outer_dim, int64_t outer_coef,
                         uint32_t inner_box, uint32_t outer_box, int nbatch, std::vector<int>* batch_axes,
@@ -676,8 +808,14 @@ KernelPlan generate_gemm(const Graph& g, const Candidate& c) {
       d->box[d->rank] = box;
       d->rank++;
     };
-    push(inner_dim, 1, inner_box);
-    push(outer_dim, outer_dim > 1 ? outer_coef : (outer_coef ? outer_coef : inner_dim), outer_box);
+    // K-split views: the K dimension (inner when K-major, outer otherwise) becomes
+    // (k % D) with its own stride plus a (k / D) dimension right after the outer one
+    const bool k_inner = inner_box == 64 && v.ksplit && (&v == &va ? a_kmaj : b_kmaj);
+    const int64_t D = v.ksplit;
+    push(k_inner ? D : inner_dim, 1, inner_box);
+    if (D && !k_inner) push(D, outer_coef, outer_box);
+    else push(outer_dim, outer_dim > 1 ? outer_coef : (outer_coef ? outer_coef : inner_dim), outer_box);
+    if (D) push(K / D, v.kout, 1);
     for (int b = 0; b < nbatch; ++b)
       if (v.coef[b] != 0 && v.shape[b] > 1) {
         if (d->rank >= 5) return false;
@@ -713,10 +851,9 @@ KernelPlan generate_gemm(const Graph& g, const Candidate& c) {
   // Launch configurations (the profiler keeps the fastest):
   //  * tile width BN: small BN spreads a skinny (small-M, weight-streaming) GEMM over more
   //    SMs, large BN maximises operand reuse;
-  //  * split-K (KS > 1) for grids far smaller than the 148 SMs: each CTA accumulates a
-  //    K-slice in TMEM, adds it into an fp32 scratch tile with red.global.add.v4.f32, and
-  //    the last CTA of the tile (arrival counter) runs the fused epilogue and re-zeroes
-  //    the scratch, so the kernel is self-cleaning across launches.
+  //  * split-K (KS > 1) for grids far smaller than the 148 SMs: a cluster of KS CTAs
+  //    accumulates the K-slices of one tile in their TMEMs and reduces them through
+  //    distributed shared memory (see the KS > 1 epilogue below).
   struct Cfg { int bn, ks; };
   std::vector<Cfg> cfgs;
   const int64_t NKt = (K + 63) / 64;
@@ -758,20 +895,41 @@ KernelPlan generate_gemm(const Graph& g, const Candidate& c) {
       continue;
     }
     if (!b_kmaj) db.swizzle = b_swz_tma;
-    const GemmEpilogue& ep = epv;
     const int A_BYTES = 128 * 64 * 2, B_BYTES = BN * 64 * 2, STAGE = A_BYTES + B_BYTES;
     const int64_t NK = NKt / KS;  // K-blocks per CTA
     // Pipeline depth: keep as many K-blocks in flight as shared memory allows (up to all
     // of them) -- small-M GEMMs are bound by TMA round-trip latency, not bandwidth.
     const int S = (int)std::max<int64_t>(2, std::min<int64_t>(NK, (200 * 1024) / STAGE));
-    const int smem = S * STAGE + 1024 + (2 * S + 1) * 8 + 16;
+    // Epilogue mapping.  KS == 1: column-lane staging unless rows are contiguous or the
+    // epilogue reduces rows.  KS > 1 (cluster split-K): the owner CTA of a row block runs
+    // the epilogue over [RO x BN] with T = BN / 8 lanes per row, straight from the
+    // DSMEM-reduced partial sums.
+    const int TE = has_reduce ? 1 : KS > 1 ? BN / 8 : epilogue_lanes(g, c, mm, CW, pre, (int64_t)S * STAGE, &epv);
+    if (KS > 1) {
+      GemmEpilogue e2;
+      if (!make_gemm_epilogue(g, c, mm, BN, pre, &e2, &err, -1, TE) || e2.ext.size() != epv.ext.size()) continue;
+      epv = e2;
+    }
+    const GemmEpilogue& ep = epv;
+    const int RO = 128 / KS, PB = BN + 4;                  // rows owned per CTA, receive pitch (floats)
+    const int64_t recv_bytes = KS > 1 ? (int64_t)128 * PB * 4 : 0;
+    const int64_t REG = std::max<int64_t>((int64_t)S * STAGE, recv_bytes);
+    if (REG + 1024 + (2 * S + 1) * 8 + 16 > 227 * 1024) continue;
+    const int smem = (int)REG + 1024 + (2 * S + 1) * 8 + 16;
     const int tcols = BN < 32 ? 32 : BN;
     const int64_t Nt = (N + BN - 1) / BN;
-    const int64_t acc_bytes = ((batch * M * N * 4) + 255) / 256 * 256;
     uint32_t idesc = (1u << 4) | (1u << 7) | (1u << 10) | ((a_kmaj ? 0u : 1u) << 15) | ((b_kmaj ? 0u : 1u) << 16) |
                      ((uint32_t)(BN >> 3) << 17) | ((uint32_t)(128 >> 4) << 24);
-    auto coords = [&](const std::string& inner, const std::string& outer, const std::vector<int>& baxes) {
-      std::string s = inner + ", " + outer;
+    // coordinates of a load: K-split views address k as (k % D, .., k / D)
+    auto coords = [&](std::string inner, std::string outer, const std::vector<int>& baxes, const View& v,
+                      bool k_inner) {
+      std::string extra;
+      if (v.ksplit) {
+        std::string& kc = k_inner ? inner : outer;
+        extra = ", (" + kc + ") / " + str(v.ksplit);
+        kc = "(" + kc + ") % " + str(v.ksplit);
+      }
+      std::string s = inner + ", " + outer + extra;
       for (int b : baxes) s += ", " + ep.batch_vars[b];
       return s;
     };
@@ -781,27 +939,60 @@ KernelPlan generate_gemm(const Graph& g, const Candidate& c) {
     for (size_t i = 0; i < kp.ext.size(); ++i)
       k << "const " << (g.dtype_of(kp.ext[i]) == DType::F32 ? "float" : "bf16_t") << "* __restrict__ p" << i << ", ";
     k << (g.prims[c.output].dtype == DType::F32 ? "float" : "bf16_t") << "* __restrict__ out, ";
-    if (KS > 1) k << "unsigned char* __restrict__ scratch, ";
     k << "const __grid_constant__ TmaMap tmA, const __grid_constant__ TmaMap tmB) {\n";
     k << "  typedef int idx_t;\n";
     k << "  extern __shared__ __align__(1024) unsigned char smem_raw[];\n";
     k << "  unsigned char* smem = (unsigned char*)(((unsigned long long)smem_raw + 1023ull) & ~1023ull);\n";
-    k << "  unsigned long long* full = (unsigned long long*)(smem + " << S * STAGE << ");\n";
+    k << "  unsigned long long* full = (unsigned long long*)(smem + " << REG << ");\n";
     k << "  unsigned long long* empty = full + " << S << ";\n";
     k << "  unsigned long long* accf = empty + " << S << ";\n";
     k << "  unsigned* tslot = (unsigned*)(accf + 1);\n";
     k << "  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;\n";
-    k << "  const int tile_m = blockIdx.x * 128, tile_n = blockIdx.y * " << BN << ";\n";
-    if (KS > 1) k << "  const int ks = blockIdx.z % " << KS << ";\n  int bzl = blockIdx.z / " << KS << ";\n";
-    else k << "  const int ks = 0;\n  int bzl = blockIdx.z;\n";
+    if (KS > 1)  // cluster of KS CTAs along x = the K-slices of one output tile
+      k << "  const int ks = blockIdx.x % " << KS << ";\n  const int tile_m = (blockIdx.x / " << KS
+        << ") * 128, tile_n = blockIdx.y * " << BN << ";\n";
+    else k << "  const int ks = 0;\n  const int tile_m = blockIdx.x * 128, tile_n = blockIdx.y * " << BN << ";\n";
+    k << "  int bzl = blockIdx.z;\n";
     k << "  const int bzlin = bzl;\n  (void)bzlin; (void)ks;\n";
     for (int b = nbC - 1; b >= 0; --b) {
       k << "  const int " << ep.batch_vars[b] << " = bzl % " << C[b] << "; bzl /= " << C[b] << ";\n";
     }
     k << "  (void)bzl;\n";
+    // operand loads (variables kb, sa, sb, s in scope)
+    std::ostringstream lda, ldb;
+    if (a_kmaj) {
+      lda << "      " << load(da.rank) << "(sa, &tmA, full + s, " << coords("kb * 64", "tile_m", ba_axes, va, true) << ");\n";
+    } else {
+      for (int cc = 0; cc < 2; ++cc)
+        lda << "      " << load(da.rank) << "(sa + " << cc * 8192 << ", &tmA, full + s, "
+            << coords("tile_m + " + str(cc * 64), "kb * 64", ba_axes, va, false) << ");\n";
+    }
+    if (b_kmaj) {
+      ldb << "      " << load(db.rank) << "(sb, &tmB, full + s, " << coords("kb * 64", "tile_n", bb_axes, vb, true) << ");\n";
+    } else {
+      for (int cc = 0; cc < (BN + 63) / 64; ++cc)
+        ldb << "      " << load(db.rank) << "(sb + " << cc * 8192 << ", &tmB, full + s, "
+            << coords("tile_n + " + str(cc * 64), "kb * 64", bb_axes, vb, false) << ");\n";
+    }
+    // Operands that are graph inputs (weights) are never written by any kernel of a plan,
+    // so their first PRE stages are fetched right after barrier init, before the
+    // programmatic-dependency wait: under PDL the weight stream of this GEMM overlaps
+    // the tail of the previous kernel.
+    const bool earlyA = va.src.is_input, earlyB = vb.src.is_input;
+    const int64_t PRE = (earlyA || earlyB) ? std::min<int64_t>(S, NK) : 0;
     k << "  if (threadIdx.x == 0) {\n    for (int s = 0; s < " << S
       << "; ++s) { mbar_init(full + s, 1); mbar_init(empty + s, 1); }\n"
-      << "    mbar_init(accf, 1);\n    mbar_fence_init();\n    tma_prefetch(&tmA);\n    tma_prefetch(&tmB);\n  }\n";
+      << "    mbar_init(accf, 1);\n    mbar_fence_init();\n    tma_prefetch(&tmA);\n    tma_prefetch(&tmB);\n";
+    if (PRE) {
+      k << "    for (int s = 0; s < " << PRE << "; ++s) {\n      const int kb = ks * " << NK << " + s;\n";
+      k << "      mbar_expect_tx(full + s, " << STAGE << "u);\n";
+      k << "      unsigned char* sa = smem + s * " << STAGE << ";\n      unsigned char* sb = sa + " << A_BYTES << ";\n";
+      k << "      (void)sa; (void)sb; (void)kb;\n";
+      if (earlyA) k << lda.str();
+      if (earlyB) k << ldb.str();
+      k << "    }\n";
+    }
+    k << "  }\n";
     k << "  if (warp == 2) tc_alloc(tslot, " << tcols << ");\n";
     k << "  tc_fence_before();\n  __syncthreads();\n  tc_fence_after();\n";
     k << "  const unsigned tmem = *tslot;\n";
@@ -810,24 +1001,13 @@ KernelPlan generate_gemm(const Graph& g, const Candidate& c) {
     k << "  if (warp == 0 && lane == 0) {\n";
     k << "    int s = 0; unsigned ph = 0;\n";
     k << "    for (int kb = ks * " << NK << "; kb < (ks + 1) * " << NK << "; ++kb) {\n";
+    k << "      const bool pre = kb - ks * " << NK << " < " << PRE << ";\n      (void)pre;\n";
     k << "      mbar_wait(empty + s, ph ^ 1u);\n";
-    k << "      mbar_expect_tx(full + s, " << STAGE << "u);\n";
+    k << "      if (!pre) mbar_expect_tx(full + s, " << STAGE << "u);\n";
     k << "      unsigned char* sa = smem + s * " << STAGE << ";\n";
     k << "      unsigned char* sb = sa + " << A_BYTES << ";\n";
-    if (a_kmaj) {
-      k << "      " << load(da.rank) << "(sa, &tmA, full + s, " << coords("kb * 64", "tile_m", ba_axes) << ");\n";
-    } else {
-      for (int cc = 0; cc < 2; ++cc)
-        k << "      " << load(da.rank) << "(sa + " << cc * 8192 << ", &tmA, full + s, "
-          << coords("tile_m + " + str(cc * 64), "kb * 64", ba_axes) << ");\n";
-    }
-    if (b_kmaj) {
-      k << "      " << load(db.rank) << "(sb, &tmB, full + s, " << coords("kb * 64", "tile_n", bb_axes) << ");\n";
-    } else {
-      for (int cc = 0; cc < (BN + 63) / 64; ++cc)
-        k << "      " << load(db.rank) << "(sb + " << cc * 8192 << ", &tmB, full + s, "
-          << coords("tile_n + " + str(cc * 64), "kb * 64", bb_axes) << ");\n";
-    }
+    k << (earlyA ? "      if (!pre) {\n" + lda.str() + "      }\n" : lda.str());
+    k << (earlyB ? "      if (!pre) {\n" + ldb.str() + "      }\n" : ldb.str());
     k << "      if (++s == " << S << ") { s = 0; ph ^= 1u; }\n    }\n";
     // MMA issuer
     k << "  } else if (warp == 1 && lane == 0) {\n";
@@ -849,57 +1029,44 @@ KernelPlan generate_gemm(const Graph& g, const Candidate& c) {
     k << "    tc_commit(accf);\n  }\n";
     // epilogue
     k << "  __syncwarp();\n  mbar_wait(accf, 0);\n  __syncwarp();\n  tc_fence_after();\n";
-    k << "  const int gm = tile_m + warp * 32 + lane;\n";
-    auto tmem_load = [&]() {
-      std::ostringstream t;
-      if (CW <= 32) {
-        t << "      tc_ld" << CW << "(tmem + ((unsigned)(warp * 32) << 16) + (unsigned)(ch * " << CW << "), acc);\n";
-      } else {
-        t << "      #pragma unroll\n      for (int q = 0; q < " << CW / 32 << "; ++q)\n"
-          << "        tc_ld32(tmem + ((unsigned)(warp * 32) << 16) + (unsigned)(ch * " << CW << " + q * 32), acc + q * 32);\n";
-      }
-      return t.str();
-    };
     if (KS == 1) {
-      k << "  {\n    const int tid = 0;\n    (void)tid;\n";
-      k << "    #pragma unroll 1\n    for (int ch = 0; ch < " << BN / CW << "; ++ch) {\n";
-      k << "      const int nb = tile_n + ch * " << CW << ";\n";
-      k << "      float acc[" << CW << "];\n";
-      k << tmem_load();
-      k << "      if (gm < " << M << " && nb < " << N << ") {\n";
-      k << ep.body << ep.store;
-      k << "      }\n    }\n  }\n";
+      k << emit_tmem_epilogue(ep, BN, CW, TE, M, N);
     } else {
-      // 1) add this K-slice's partial tile into the fp32 scratch tile (L2 reductions)
-      k << "  float* wsa = reinterpret_cast<float*>(scratch) + (size_t)bzlin * " << M * N << ";\n";
-      k << "  unsigned* cnt = reinterpret_cast<unsigned*>(scratch + " << acc_bytes << ");\n";
-      k << "  const int tile_id = (bzlin * " << Nt << " + blockIdx.y) * " << Mt << " + blockIdx.x;\n";
-      k << "  #pragma unroll 1\n  for (int ch = 0; ch < " << BN / CW << "; ++ch) {\n";
-      k << "    float acc[" << CW << "];\n";
-      k << tmem_load();
-      k << "    if (gm < " << M << ") {\n      float* dst = wsa + (size_t)gm * " << N << " + tile_n + ch * " << CW << ";\n";
-      k << "      #pragma unroll\n      for (int q = 0; q < " << CW / 4 << "; ++q)\n";
-      k << "        asm volatile(\"red.global.add.v4.f32 [%0], {%1, %2, %3, %4};\" :: \"l\"(dst + 4 * q), "
-           "\"f\"(acc[4 * q]), \"f\"(acc[4 * q + 1]), \"f\"(acc[4 * q + 2]), \"f\"(acc[4 * q + 3]) : \"memory\");\n";
-      k << "    }\n  }\n";
-      // 2) the last CTA of this tile runs the epilogue on the full sum and re-zeroes it
-      k << "  __shared__ unsigned is_last;\n";
-      k << "  __threadfence();\n  __syncthreads();\n";
-      k << "  if (threadIdx.x == 0) is_last = atomicAdd(cnt + tile_id, 1u) == " << KS - 1 << "u;\n";
-      k << "  __syncthreads();\n";
-      k << "  if (is_last) {\n    __threadfence();\n    const int tid = 0;\n    (void)tid;\n";
+      // Cluster split-K: the KS CTAs of a cluster hold K-slice partials of one tile in
+      // TMEM.  (1) cluster barrier: every CTA's MMAs are done, so every operand ring is
+      // idle and becomes a receive buffer [KS slots][RO rows][BN (+4 pad)] fp32;
+      // (2) each thread pushes its accumulator row into the owner CTA of that row
+      // (rows [o*RO, (o+1)*RO) belong to rank o) with st.shared::cluster; (3) cluster
+      // barrier (release/acquire); (4) each CTA sums the KS slots of its RO rows and runs
+      // the fused epilogue, T = BN/8 lanes per row (coalesced side reads and stores).
+      // No global scratch, no atomics, nothing to re-zero.
+      k << "  cluster_sync();\n";
+      k << "  {\n    const int r = warp * 32 + lane;\n";
+      k << "    const unsigned dst = cluster_map(smem_u32(smem) + (unsigned)((ks * " << RO << " + r % " << RO << ") * "
+        << PB * 4 << "), (unsigned)(r / " << RO << "));\n";
       k << "    #pragma unroll 1\n    for (int ch = 0; ch < " << BN / CW << "; ++ch) {\n";
-      k << "      const int nb = tile_n + ch * " << CW << ";\n";
-      k << "      float acc[" << CW << "];\n";
-      k << "      if (gm < " << M << ") {\n";
-      k << "        float* src = wsa + (size_t)gm * " << N << " + nb;\n";
-      k << "        #pragma unroll\n        for (int q = 0; q < " << CW / 4 << "; ++q) {\n";
-      k << "          const float4 t4 = __ldcg(reinterpret_cast<const float4*>(src + 4 * q));\n";
-      k << "          acc[4 * q] = t4.x; acc[4 * q + 1] = t4.y; acc[4 * q + 2] = t4.z; acc[4 * q + 3] = t4.w;\n";
-      k << "          __stcg(reinterpret_cast<float4*>(src + 4 * q), make_float4(0.f, 0.f, 0.f, 0.f));\n        }\n";
-      k << ep.body << ep.store;
-      k << "      }\n    }\n";
-      k << "    if (threadIdx.x == 0) cnt[tile_id] = 0u;\n  }\n";
+      k << "      float accr[" << CW << "];\n";
+      k << "      tc_ld" << CW << "(tmem + ((unsigned)(warp * 32) << 16) + (unsigned)(ch * " << CW << "), accr);\n";
+      k << "      #pragma unroll\n      for (int q = 0; q < " << CW / 4 << "; ++q)\n";
+      k << "        st_cluster_v4(dst + (unsigned)((ch * " << CW << " + 4 * q) * 4), accr[4 * q], accr[4 * q + 1], "
+           "accr[4 * q + 2], accr[4 * q + 3]);\n";
+      k << "    }\n  }\n";
+      k << "  cluster_sync();\n";
+      k << "  {\n    const float* recv = reinterpret_cast<const float*>(smem);\n";
+      k << "    #pragma unroll\n    for (int it = threadIdx.x; it < " << RO * TE << "; it += 128) {\n";
+      k << "      const int rl = it / " << TE << ", tid = it % " << TE << ";\n";
+      k << "      const int gmr = tile_m + ks * " << RO << " + rl;\n";
+      k << "      const int gm = gmr < " << M << " ? gmr : " << M - 1 << ";\n";
+      k << "      const int nb = tile_n;\n";
+      k << "      float acc[8];\n";
+      k << "      #pragma unroll\n      for (int e = 0; e < 8; ++e) acc[e] = 0.f;\n";
+      k << "      #pragma unroll\n      for (int sl = 0; sl < " << KS << "; ++sl) {\n";
+      k << "        const float* src = recv + (sl * " << RO << " + rl) * " << PB << " + tid * 8;\n";
+      k << "        const float4 a0 = *reinterpret_cast<const float4*>(src), a1 = *reinterpret_cast<const float4*>(src + 4);\n";
+      k << "        acc[0] += a0.x; acc[1] += a0.y; acc[2] += a0.z; acc[3] += a0.w;\n";
+      k << "        acc[4] += a1.x; acc[5] += a1.y; acc[6] += a1.z; acc[7] += a1.w;\n      }\n";
+      k << "      {\n" << ep.body << "      if (gmr < " << M << ") {\n" << ep.store << "      }\n      }\n";
+      k << "    }\n  }\n";
     }
     k << "  tc_fence_before();\n  __syncthreads();\n";
     k << "  if (warp == 2) tc_dealloc(tmem, " << tcols << ");\n}\n";
@@ -915,17 +1082,18 @@ KernelPlan generate_gemm(const Graph& g, const Candidate& c) {
     kv.source = src;
     kv.tcgen05 = true;
     kv.block = 128;
-    kv.grid = Mt;
+    kv.grid = Mt * KS;
     kv.grid_y = Nt;
-    kv.grid_z = batch * KS;
+    kv.grid_z = batch;
+    kv.cluster = KS;
     kv.smem = smem;
-    if (KS > 1) kv.scratch_bytes = acc_bytes + Mt * Nt * batch * 4;
     da.tensor = slotA;
     db.tensor = slotB;
     kv.tma = {da, db};
     std::ostringstream t;
     t << "gemm BM=128 BN=" << BN << " BK=64 splitK=" << KS << " stages=" << S << " A=" << (a_kmaj ? "K" : "M")
-      << "-major B=" << (b_kmaj ? "K" : "N") << "-major M=" << M << " N=" << N << " K=" << K << " batch=" << batch;
+      << "-major B=" << (b_kmaj ? "K" : "N") << "-major M=" << M << " N=" << N << " K=" << K << " batch=" << batch
+      << (TE > 1 ? " epi=cl" : "");
     kv.tag = t.str();
     kp.variants.push_back(kv);
   }
@@ -973,7 +1141,10 @@ KernelPlan generate_attention(const Graph& g, const Candidate& c) {
     return kp;
   }
   for (auto* v : {&vq, &vk, &vv})
-    if (g.dtype_of(v->src) != DType::BF16 || (v->off * 2) % 16) { kp.reject = "attention operands must be aligned bf16"; return kp; }
+    if (g.dtype_of(v->src) != DType::BF16 || (v->off * 2) % 16 || v->ksplit) {
+      kp.reject = "attention operands must be aligned, unsplit bf16 views";
+      return kp;
+    }
   const Shape& SS = L1.shape;  // [batch..., M, N1]
   const Shape& OS = L2.shape;  // [batch..., M, N2]
   int nb = (int)SS.size() - 2;
@@ -994,6 +1165,16 @@ KernelPlan generate_attention(const Graph& g, const Candidate& c) {
   GemmEpilogue ep1, ep2;
   if (!make_gemm_epilogue(g, c, lin[0], (int)N1, pre, &ep1, &err, pnode)) { kp.reject = "P: " + err; return kp; }
   if (!make_gemm_epilogue(g, c, lin[1], 32, ep1.ext, &ep2, &err)) { kp.reject = "O: " + err; return kp; }
+  // column-lane O epilogue unless O is stored row-contiguous
+  int TE2 = 1;
+  if (!ep2.rows_unit) {
+    GemmEpilogue e2;
+    std::string e;
+    if (make_gemm_epilogue(g, c, lin[1], 32, ep1.ext, &e2, &e, -1, 4) && e2.ext.size() == ep2.ext.size()) {
+      ep2 = e2;
+      TE2 = 4;
+    }
+  }
   kp.ext = ep2.ext;
   auto slot_of = [&](const Ref& r) {
     for (size_t i = 0; i < kp.ext.size(); ++i)
@@ -1055,14 +1236,15 @@ KernelPlan generate_attention(const Graph& g, const Candidate& c) {
   k << "  extern __shared__ __align__(1024) unsigned char smem_raw[];\n";
   k << "  unsigned char* smem = (unsigned char*)(((unsigned long long)smem_raw + 1023ull) & ~1023ull);\n";
   k << "  unsigned long long* bars = (unsigned long long*)(smem + " << offB << ");\n";
-  k << "  unsigned long long *ldf = bars, *sfull = bars + 1, *pfull = bars + 2, *ofull = bars + 3;\n";
-  k << "  unsigned* tslot = (unsigned*)(bars + 4);\n";
+  k << "  unsigned long long *ldf = bars, *sfull = bars + 1, *pfull = bars + 2, *ofull = bars + 3, *ldv = bars + 4;\n";
+  k << "  unsigned* tslot = (unsigned*)(bars + 5);\n";
   k << "  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;\n";
   k << "  const int tile_m = blockIdx.x * 128;\n";
   k << "  int bzl = blockIdx.z;\n";
   for (int b = nb - 1; b >= 0; --b) k << "  const int bz" << b << " = bzl % " << SS[b] << "; bzl /= " << SS[b] << ";\n";
   k << "  (void)bzl;\n";
   k << "  if (threadIdx.x == 0) {\n    mbar_init(ldf, 1); mbar_init(sfull, 1); mbar_init(pfull, 4); mbar_init(ofull, 1);\n"
+    << "    mbar_init(ldv, 1);\n"
     << "    mbar_fence_init();\n    tma_prefetch(&tmQ); tma_prefetch(&tmK); tma_prefetch(&tmV);\n  }\n";
   k << "  if (warp == 5) tc_alloc(tslot, " << tcols << ");\n";
   k << "  tc_fence_before();\n  __syncthreads();\n  tc_fence_after();\n";
@@ -1070,17 +1252,19 @@ KernelPlan generate_attention(const Graph& g, const Candidate& c) {
   k << "  pdl_trigger();\n  pdl_wait();\n";
   // TMA: warp 4
   k << "  if (warp == 4 && lane == 0) {\n";
-  k << "    mbar_expect_tx(ldf, " << Q_BYTES + K_BYTES + V_BYTES << "u);\n";
+  // Q and K on one barrier, V on its own: S = QK^T and the softmax overlap V's arrival
+  k << "    mbar_expect_tx(ldf, " << Q_BYTES + K_BYTES << "u);\n";
+  k << "    mbar_expect_tx(ldv, " << V_BYTES << "u);\n";
   for (int64_t kb = 0; kb < KB1; ++kb) {
     k << "    " << load(dq.rank) << "(smem + " << kb * 16384 << ", &tmQ, ldf, " << coords(std::to_string(kb * 64), "tile_m", bq) << ");\n";
     k << "    " << load(dk.rank) << "(smem + " << offK + kb * N1 * 128 << ", &tmK, ldf, " << coords(std::to_string(kb * 64), "0", bk) << ");\n";
   }
   if (v_n) {
     for (int64_t cc = 0; cc < (N2 + 63) / 64; ++cc)
-      k << "    " << load(dv.rank) << "(smem + " << offV + cc * N1 * 128 << ", &tmV, ldf, " << coords(std::to_string(cc * 64), "0", bv) << ");\n";
+      k << "    " << load(dv.rank) << "(smem + " << offV + cc * N1 * 128 << ", &tmV, ldv, " << coords(std::to_string(cc * 64), "0", bv) << ");\n";
   } else {
     for (int64_t cc = 0; cc < N1 / 64; ++cc)
-      k << "    " << load(dv.rank) << "(smem + " << offV + cc * N2 * 128 << ", &tmV, ldf, " << coords(std::to_string(cc * 64), "0", bv) << ");\n";
+      k << "    " << load(dv.rank) << "(smem + " << offV + cc * N2 * 128 << ", &tmV, ldv, " << coords(std::to_string(cc * 64), "0", bv) << ");\n";
   }
   // MMA: warp 5
   k << "  } else if (warp == 5 && lane == 0) {\n";
@@ -1091,7 +1275,7 @@ KernelPlan generate_attention(const Graph& g, const Candidate& c) {
   k << "        tc_mma(tmem, umma_desc(sq + kb * 16384 + k * 32, 16, 1024), umma_desc(sk + kb * " << N1 * 128
     << " + k * 32, 16, 1024), " << id1 << "u, (kb | k) != 0);\n";
   k << "    tc_commit(sfull);\n";
-  k << "    mbar_wait(pfull, 0);\n    tc_fence_after();\n";
+  k << "    mbar_wait(pfull, 0);\n    mbar_wait(ldv, 0);\n    tc_fence_after();\n";
   k << "    #pragma unroll\n    for (int k0 = 0; k0 < " << N1 << "; k0 += 16) {\n";
   k << "      const unsigned long long ad = umma_desc(sp + (k0 >> 6) * 16384 + (k0 & 63) * 2, 16, 1024);\n";
   if (v_n)
@@ -1119,12 +1303,11 @@ KernelPlan generate_attention(const Graph& g, const Candidate& c) {
   k << "    }\n";
   k << "    fence_async_smem();\n    tc_fence_before();\n    __syncwarp();\n    if (lane == 0) mbar_arrive(pfull);\n";
   k << "    mbar_wait(ofull, 0);\n    __syncwarp();\n    tc_fence_after();\n";
-  k << "    #pragma unroll 1\n    for (int ch = 0; ch < " << (N2 + 31) / 32 << "; ++ch) {\n";
-  k << "      const int nb = ch * 32;\n      float acc[32];\n";
-  k << "      tc_ld32(tmem + ((unsigned)(warp * 32) << 16) + (unsigned)(" << N1 << " + ch * 32), acc);\n";
-  k << "      if (gm < " << M << " && nb < " << N2 << ") {\n";
-  k << ep2.body << ep2.store;
-  k << "      }\n    }\n  }\n";
+  // O epilogue: Q/K/V/P shared memory is idle now (both MMAs done) and serves as the
+  // column-lane staging buffer
+  k << "    const int tile_n = 0;\n    const unsigned tmem_o = tmem + " << N1 << ";\n";
+  k << "  " << emit_tmem_epilogue(ep2, (int)((N2 + 31) / 32 * 32), 32, TE2, M, N2, "tmem_o");
+  k << "  }\n";
   k << "  tc_fence_before();\n  __syncthreads();\n";
   k << "  if (warp == 5) tc_dealloc(tmem, " << tcols << ");\n}\n";
   KernelVariant kv;

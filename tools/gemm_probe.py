@@ -50,7 +50,9 @@ def main():
             tags = []
             for v in range(nv):
                 kg.set_variant(c["index"], v)
-                tags.append(kg.variant_info(c["index"])[2].split(" M=")[0].replace("gemm BM=128 ", ""))
+                t = kg.variant_info(c["index"])[2]
+                tags.append(t.split(" M=")[0].replace("gemm BM=128 ", "").replace(" BK=64", "")
+                            .replace(" A=K-major B=N-major", "") + (" cl" if "epi=cl" in t else ""))
             kg.set_variant(c["index"], best)
             row = "  ".join(f"{t}:{ns}" for t, ns in sorted(zip(tags, vc), key=lambda z: z[1]))
             print(f"M={m} K={k} N={n} members={c['members']} best={costs[c['index']]} ns | {row}")
