@@ -311,7 +311,7 @@ def scaled_variant(K, pk, global_batch=64, steps=10, coll_dev=None):
         gather_ms = (time.perf_counter() - t1) / 3 * 1e3
     order = kg.plan()
     dom = max(order, key=lambda i: costs[i])
-    cold = kg.profile([dom], flush_l2=True, trials=7)[0]
+    cold = kg.profile([dom], flush_l2=True, trials=7, tune=False)[0]
     dc = cands[dom]
     flops = sum(cands[i]["flops"] for i in order)
     res = {"workload": f"C2 ViT-B MHSA layer, global batch {global_batch} x seq 128 sharded over {ws_} GPU(s), "
@@ -321,7 +321,7 @@ def scaled_variant(K, pk, global_batch=64, steps=10, coll_dev=None):
            "tflops_plan": flops / (ms * 1e-3) / 1e12, "tune_s": t_tune, "output_gather_ms_host_timed": gather_ms,
            "plan_members": [cands[i]["members"] for i in order],
            "dominant": {"candidate": dom, "class": dc["klass"], "members": len(dc["members"]),
-                        "ns_cold_l2": cold, "variant": kg.variant_info(dom)[2], "name": dc["signature"]}}
+                        "ns_cold_l2": cold, "variant": kg.variant_info(dom)[2], "name": kg.kernel_name(dom)}}
     if dc["flops"] > 0:
         t = dc["flops"] / (cold * 1e-9) / 1e12
         res["dominant"].update({"bound": "tensor", "achieved_tflops": t, "peak_tflops": pk["bf16_tflops"],
@@ -587,7 +587,7 @@ def main():
 
     # dominant kernel: largest profiled cost in the plan; re-time it cold-L2 on its stream
     dom = max(order, key=lambda i: costs[i])
-    dom_cold = kg.profile([dom], flush_l2=True, trials=9)[0]
+    dom_cold = kg.profile([dom], flush_l2=True, trials=9, tune=False)[0]
     dc = cands[dom]
     if dc["klass"] == "gemm" and dc["flops"] > 0:
         # compute-class kernel: report against the bf16 tensor peak if it is compute bound
@@ -602,10 +602,11 @@ def main():
         ach = dc["bytes"] / (dom_cold * 1e-9) / 1e9
         roof = {"bound": "hbm", "achieved": ach, "peak": pk["hbm_gbs"], "unit": "GB/s"}
     roof["frac"] = roof["achieved"] / roof["peak"]
-    roof["traffic"] = load_ncu_traffic(dc["signature"])
+    kname = kg.kernel_name(dom)
+    roof["traffic"] = load_ncu_traffic(kname)
     roof["kernel"] = {"candidate": dom, "class": dc["klass"], "members": len(dc["members"]),
                       "algorithmic_bytes": dc["bytes"], "flops": dc["flops"], "ns_cold_l2": dom_cold,
-                      "ns_warm": costs[dom], "name": dc["signature"], "peak_source": pk["source"]}
+                      "ns_warm": costs[dom], "name": kname, "peak_source": pk["source"]}
 
     # plan roofline: T*(u) = sum_i max(B_i / BW, F_i / P) over the selected
     # kernels, and the launch floor n_kernels * t_min + T*(u), t_min = the cheapest profiled

@@ -117,6 +117,14 @@ class KorchGraph:
         check(LIB.korch_candidate_source(self.h, i, buf, len(buf), C.byref(need)))
         return buf.value.decode()
 
+    def kernel_name(self, i: int) -> str:
+        """Name of the chosen (else first) launch variant's kernel of candidate i (the name
+        ncu reports)."""
+        import re
+        _, ch, _ = self.variant_info(i)
+        names = re.findall(r"__global__ void __launch_bounds__\([^)]*\) (korch_\w+)\(", self.source(i))
+        return names[max(ch, 0)] if names else ""
+
     def generable(self):
         return [c["index"] for c in self.cands if c["klass"] != "rejected"]
 

@@ -52,19 +52,31 @@ KernelPlan generate_kernel(const Graph& g, const Candidate& c);
 
 // Epilogue of a GEMM candidate, emitted by the row-template machinery: `body` computes
 // the output chunk from float acc[32] (row gm, columns nb..nb+31) and `store` writes it.
+// A full-tile side input of a GEMM epilogue (e.g. the residual of x + W.h) whose view is
+// affine: element (gm, j) at off + gm * sm + j (+ batch terms).  The GEMM kernel stages
+// the [128 x BN] tile by TMA into shared memory during the main loop; the epilogue reads
+// it from there (`sside<i>` = its shared address, row pitch BN elements).
+struct EpiSide {
+  int slot = -1;                       // index into GemmEpilogue::ext
+  int64_t off = 0, sm = 0;             // elements
+  std::vector<int64_t> bcoef;          // per GEMM batch axis (elements)
+  int dtype = 1;                       // 0 = f32, 1 = bf16
+};
+
 struct GemmEpilogue {
   std::vector<Ref> ext;               // pre_ext first, then epilogue operands
   std::string body, store;
   int64_t bytes = 0;                  // epilogue reads + output write
   std::vector<std::string> batch_vars;
   bool rows_unit = false;             // output address has unit stride along the row gm
+  std::vector<EpiSide> sides;         // side inputs read from TMA-staged tiles (stage_bn > 0)
 };
 // t > 1: t threads share each row chunk (column-lane epilogue, see gemm_gen.cpp); the
 // body then reads float acc[cw / t] for columns nb + (tid + k*t)*8 + [0, 8).
 // target >= 0: compute that intermediate node instead of the candidate's output; then
 // `store` holds the name of the float[cw] array with its values (no global store).
 bool make_gemm_epilogue(const Graph& g, const Candidate& c, int mm, int cw, const std::vector<Ref>& pre_ext,
-                        GemmEpilogue* out, std::string* err, int target = -1, int t = 1);
+                        GemmEpilogue* out, std::string* err, int target = -1, int t = 1, int stage_bn = 0);
 // Prologue of a GEMM whose A operand is computed in the kernel (e.g. LayerNorm feeding a
 // Linear): `body` runs once per A row (local row r, global row gm; one warp per row,
 // lane = tid) and writes the bf16 row into the resident, 128B-swizzled K-major A tile at

@@ -216,13 +216,13 @@ static std::string emit_tmem_epilogue(const GemmEpilogue& ep, int BN, int CW, in
 // Column-lane epilogue choice: T = CW / 8 lanes per row unless the output is contiguous
 // along rows (then the row mapping already stores coalesced) or the epilogue reduces rows.
 static int epilogue_lanes(const Graph& g, const Candidate& c, int mm, int CW, const std::vector<Ref>& pre,
-                          int64_t ring_bytes, GemmEpilogue* ep) {
+                          int64_t ring_bytes, GemmEpilogue* ep, int stage_bn = 0) {
   if (ep->rows_unit || CW % 8 || CW > 32 || stage_bytes(CW) > ring_bytes) return 1;
   for (int m : c.members)
     if (g.prims[m].kind == Kind::Reduce) return 1;
   GemmEpilogue e2;
   std::string err;
-  if (!make_gemm_epilogue(g, c, mm, CW, pre, &e2, &err, -1, CW / 8)) return 1;
+  if (!make_gemm_epilogue(g, c, mm, CW, pre, &e2, &err, -1, CW / 8, stage_bn)) return 1;
   if (e2.ext.size() != ep->ext.size()) return 1;
   *ep = e2;
   return CW / 8;
@@ -899,23 +899,74 @@ KernelPlan generate_gemm(const Graph& g, const Candidate& c) {
     const int64_t NK = NKt / KS;  // K-blocks per CTA
     // Pipeline depth: keep as many K-blocks in flight as shared memory allows (up to all
     // of them) -- small-M GEMMs are bound by TMA round-trip latency, not bandwidth.
-    const int S = (int)std::max<int64_t>(2, std::min<int64_t>(NK, (200 * 1024) / STAGE));
+    int S = (int)std::max<int64_t>(2, std::min<int64_t>(NK, (200 * 1024) / STAGE));
     // Epilogue mapping.  KS == 1: column-lane staging unless rows are contiguous or the
     // epilogue reduces rows.  KS > 1 (cluster split-K): the owner CTA of a row block runs
     // the epilogue over [RO x BN] with T = BN / 8 lanes per row, straight from the
     // DSMEM-reduced partial sums.
-    const int TE = has_reduce ? 1 : KS > 1 ? BN / 8 : epilogue_lanes(g, c, mm, CW, pre, (int64_t)S * STAGE, &epv);
+    // KS == 1 column-lane epilogues stage full-tile affine side inputs (residuals) by TMA
+    // into shared memory during the main loop (EpiSide): the epilogue then reads them
+    // from shared memory instead of waiting on one global round trip per pass.
+    const int TE = has_reduce ? 1
+                   : KS > 1   ? BN / 8
+                              : epilogue_lanes(g, c, mm, CW, pre, (int64_t)S * STAGE, &epv, BN <= 256 ? BN : 0);
     if (KS > 1) {
       GemmEpilogue e2;
       if (!make_gemm_epilogue(g, c, mm, BN, pre, &e2, &err, -1, TE) || e2.ext.size() != epv.ext.size()) continue;
       epv = e2;
     }
+    std::vector<int64_t> side_off;
+    int64_t side_bytes = 0;
+    for (auto& sd : epv.sides) {
+      side_off.push_back(side_bytes);
+      side_bytes += ((int64_t)128 * BN * (sd.dtype ? 2 : 4) + 1023) / 1024 * 1024;
+    }
+    if (side_bytes) {
+      const int S2 = (int)std::max<int64_t>(2, std::min<int64_t>(NK, (200 * 1024 - side_bytes) / STAGE));
+      if ((int64_t)S2 * STAGE + side_bytes > 208 * 1024) {  // no room: plain global side reads
+        GemmEpilogue e2;
+        if (!make_gemm_epilogue(g, c, mm, CW, pre, &e2, &err, -1, TE) || e2.ext.size() != epv.ext.size()) continue;
+        epv = e2;
+        side_off.clear();
+        side_bytes = 0;
+      } else {
+        S = S2;
+      }
+    }
     const GemmEpilogue& ep = epv;
     const int RO = 128 / KS, PB = BN + 4;                  // rows owned per CTA, receive pitch (floats)
     const int64_t recv_bytes = KS > 1 ? (int64_t)128 * PB * 4 : 0;
-    const int64_t REG = std::max<int64_t>((int64_t)S * STAGE, recv_bytes);
-    if (REG + 1024 + (2 * S + 1) * 8 + 16 > 227 * 1024) continue;
-    const int smem = (int)REG + 1024 + (2 * S + 1) * 8 + 16;
+    const int64_t REG0 = std::max<int64_t>((int64_t)S * STAGE, recv_bytes);
+    const int64_t REG = REG0 + side_bytes;                 // ring (| DSMEM receive) | side tiles
+    std::vector<TmaDesc> sdesc;
+    std::vector<std::vector<int>> sd_axes;
+    bool side_ok = true;
+    for (auto& sd : ep.sides) {
+      TmaDesc d;
+      d.tensor = sd.slot;
+      d.dtype = sd.dtype;
+      d.swizzle = 0;
+      d.elem_off = sd.off;
+      const int esz = sd.dtype ? 2 : 4;
+      auto push = [&](int64_t dim, int64_t st_el, uint32_t box) {
+        d.dims[d.rank] = dim; d.strides[d.rank] = st_el * esz; d.box[d.rank] = box; d.rank++;
+      };
+      push(N, 1, (uint32_t)BN);
+      push(M, sd.sm, 128);
+      std::vector<int> ax;
+      for (int b = 0; b < nbC; ++b)
+        if (sd.bcoef[b] != 0 && C[b] > 1) {
+          if (d.rank >= 5) side_ok = false;
+          else { push(C[b], sd.bcoef[b], 1); ax.push_back(b); }
+        }
+      for (int i = 1; i < d.rank; ++i)
+        if (d.strides[i] % 16 || d.strides[i] <= 0 || d.strides[i] >= (1LL << 40)) side_ok = false;
+      sdesc.push_back(d);
+      sd_axes.push_back(ax);
+    }
+    if (!side_ok) continue;
+    if (REG + 1024 + (2 * S + 2) * 8 + 16 > 227 * 1024) continue;
+    const int smem = (int)REG + 1024 + (2 * S + 2) * 8 + 16;
     const int tcols = BN < 32 ? 32 : BN;
     const int64_t Nt = (N + BN - 1) / BN;
     uint32_t idesc = (1u << 4) | (1u << 7) | (1u << 10) | ((a_kmaj ? 0u : 1u) << 15) | ((b_kmaj ? 0u : 1u) << 16) |
@@ -939,14 +990,17 @@ KernelPlan generate_gemm(const Graph& g, const Candidate& c) {
     for (size_t i = 0; i < kp.ext.size(); ++i)
       k << "const " << (g.dtype_of(kp.ext[i]) == DType::F32 ? "float" : "bf16_t") << "* __restrict__ p" << i << ", ";
     k << (g.prims[c.output].dtype == DType::F32 ? "float" : "bf16_t") << "* __restrict__ out, ";
-    k << "const __grid_constant__ TmaMap tmA, const __grid_constant__ TmaMap tmB) {\n";
+    k << "const __grid_constant__ TmaMap tmA, const __grid_constant__ TmaMap tmB";
+    for (size_t i = 0; i < sdesc.size(); ++i) k << ", const __grid_constant__ TmaMap tmS" << i;
+    k << ") {\n";
     k << "  typedef int idx_t;\n";
     k << "  extern __shared__ __align__(1024) unsigned char smem_raw[];\n";
     k << "  unsigned char* smem = (unsigned char*)(((unsigned long long)smem_raw + 1023ull) & ~1023ull);\n";
     k << "  unsigned long long* full = (unsigned long long*)(smem + " << REG << ");\n";
     k << "  unsigned long long* empty = full + " << S << ";\n";
     k << "  unsigned long long* accf = empty + " << S << ";\n";
-    k << "  unsigned* tslot = (unsigned*)(accf + 1);\n";
+    k << "  unsigned long long* sidef = accf + 1;\n  (void)sidef;\n";
+    k << "  unsigned* tslot = (unsigned*)(accf + 2);\n";
     k << "  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;\n";
     if (KS > 1)  // cluster of KS CTAs along x = the K-slices of one output tile
       k << "  const int ks = blockIdx.x % " << KS << ";\n  const int tile_m = (blockIdx.x / " << KS
@@ -980,9 +1034,24 @@ KernelPlan generate_gemm(const Graph& g, const Candidate& c) {
     // the tail of the previous kernel.
     const bool earlyA = va.src.is_input, earlyB = vb.src.is_input;
     const int64_t PRE = (earlyA || earlyB) ? std::min<int64_t>(S, NK) : 0;
+    // side tiles: one barrier for all of them; graph inputs load before the PDL wait
+    auto side_load = [&](size_t i) {
+      std::string c2 = "tile_n, tile_m";
+      for (int b : sd_axes[i]) c2 += ", " + ep.batch_vars[b];
+      return "    tma_load_" + std::to_string(sdesc[i].rank) + "d(smem + " + str(REG0 + side_off[i]) + ", &tmS" +
+             std::to_string(i) + ", sidef, " + c2 + ");\n";
+    };
     k << "  if (threadIdx.x == 0) {\n    for (int s = 0; s < " << S
       << "; ++s) { mbar_init(full + s, 1); mbar_init(empty + s, 1); }\n"
-      << "    mbar_init(accf, 1);\n    mbar_fence_init();\n    tma_prefetch(&tmA);\n    tma_prefetch(&tmB);\n";
+      << "    mbar_init(accf, 1);\n    mbar_init(sidef, 1);\n    mbar_fence_init();\n    tma_prefetch(&tmA);\n"
+      << "    tma_prefetch(&tmB);\n";
+    if (!sdesc.empty()) {
+      int64_t tot = 0;
+      for (auto& d : sdesc) tot += (int64_t)d.box[0] * d.box[1] * (d.dtype ? 2 : 4);
+      k << "    mbar_expect_tx(sidef, " << tot << "u);\n";
+      for (size_t i = 0; i < sdesc.size(); ++i)
+        if (ep.ext[ep.sides[i].slot].is_input) k << side_load(i);
+    }
     if (PRE) {
       k << "    for (int s = 0; s < " << PRE << "; ++s) {\n      const int kb = ks * " << NK << " + s;\n";
       k << "      mbar_expect_tx(full + s, " << STAGE << "u);\n";
@@ -999,6 +1068,8 @@ KernelPlan generate_gemm(const Graph& g, const Candidate& c) {
     k << "  pdl_trigger();\n  pdl_wait();\n";
     // producer
     k << "  if (warp == 0 && lane == 0) {\n";
+    for (size_t i = 0; i < sdesc.size(); ++i)
+      if (!ep.ext[ep.sides[i].slot].is_input) k << side_load(i);
     k << "    int s = 0; unsigned ph = 0;\n";
     k << "    for (int kb = ks * " << NK << "; kb < (ks + 1) * " << NK << "; ++kb) {\n";
     k << "      const bool pre = kb - ks * " << NK << " < " << PRE << ";\n      (void)pre;\n";
@@ -1030,6 +1101,11 @@ KernelPlan generate_gemm(const Graph& g, const Candidate& c) {
     // epilogue
     k << "  __syncwarp();\n  mbar_wait(accf, 0);\n  __syncwarp();\n  tc_fence_after();\n";
     if (KS == 1) {
+      if (!sdesc.empty()) {
+        for (size_t i = 0; i < sdesc.size(); ++i)
+          k << "  const unsigned sside" << i << " = smem_u32(smem + " << REG0 + side_off[i] << ");\n";
+        k << "  mbar_wait(sidef, 0);\n";
+      }
       k << emit_tmem_epilogue(ep, BN, CW, TE, M, N);
     } else {
       // Cluster split-K: the KS CTAs of a cluster hold K-slice partials of one tile in
@@ -1090,10 +1166,11 @@ KernelPlan generate_gemm(const Graph& g, const Candidate& c) {
     da.tensor = slotA;
     db.tensor = slotB;
     kv.tma = {da, db};
+    for (auto& d : sdesc) kv.tma.push_back(d);
     std::ostringstream t;
     t << "gemm BM=128 BN=" << BN << " BK=64 splitK=" << KS << " stages=" << S << " A=" << (a_kmaj ? "K" : "M")
       << "-major B=" << (b_kmaj ? "K" : "N") << "-major M=" << M << " N=" << N << " K=" << K << " batch=" << batch
-      << (TE > 1 ? " epi=cl" : "");
+      << (TE > 1 ? " epi=cl" : "") << (sdesc.empty() ? "" : " side=tma");
     kv.tag = t.str();
     kp.variants.push_back(kv);
   }

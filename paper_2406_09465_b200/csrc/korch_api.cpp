@@ -665,7 +665,12 @@ korch_status korch_profile(korch_graph* G, const int64_t* idx, int64_t n, const 
       if (s.plan.klass == KORCH_CLASS_REJECTED) { s.cost_ns = INT64_MAX; continue; }
       // Candidates whose generated kernels are identical (same source => same shapes,
       // strides and launch configuration) share one measurement.
-      int nv0 = tune ? (int)s.plan.variants.size() : 1;
+      // variants to time: all of them when tuning; otherwise only the chosen one (the
+      // first if none was chosen yet), and the choice is left as it is
+      std::vector<int> vis;
+      if (tune) for (int vi = 0; vi < (int)s.plan.variants.size(); ++vi) vis.push_back(vi);
+      else vis.push_back(s.best >= 0 ? s.best : 0);
+      const int keep_best = s.best;
       auto tkey = [&](int vi) {
         const KernelVariant& v = s.plan.variants[vi];
         return v.name + "|" + std::to_string(flush) + "|" + std::to_string(flush ? 1 : launches) + "|" +
@@ -674,18 +679,18 @@ korch_status korch_profile(korch_graph* G, const int64_t* idx, int64_t n, const 
       {
         bool all_cached = true;
         std::lock_guard<std::mutex> lk(ctx->mu);
-        for (int vi = 0; vi < nv0 && all_cached; ++vi)
+        for (int vi : vis)
           if (!ctx->timings.count(tkey(vi))) all_cached = false;
         if (all_cached) {
-          s.var_ns.assign(s.plan.variants.size(), -1);
+          if (tune || s.var_ns.size() != s.plan.variants.size()) s.var_ns.assign(s.plan.variants.size(), -1);
           int64_t best = INT64_MAX;
           int bestv = -1;
-          for (int vi = 0; vi < nv0; ++vi) {
+          for (int vi : vis) {
             int64_t ns = ctx->timings[tkey(vi)];
             s.var_ns[vi] = ns;
             if (ns < best) { best = ns; bestv = vi; }
           }
-          s.best = bestv;
+          s.best = tune || keep_best < 0 ? bestv : keep_best;
           s.cost_ns = best;
           cost[k] = best;
           continue;
@@ -713,9 +718,8 @@ korch_status korch_profile(korch_graph* G, const int64_t* idx, int64_t n, const 
       void* outp = (void*)(base + out_off);
       int64_t best = INT64_MAX;
       int bestv = -1;
-      int nv = tune ? (int)s.plan.variants.size() : 1;
-      s.var_ns.assign(s.plan.variants.size(), -1);
-      for (int vi = 0; vi < nv; ++vi) {
+      if (tune || s.var_ns.size() != s.plan.variants.size()) s.var_ns.assign(s.plan.variants.size(), -1);
+      for (int vi : vis) {
         Module* m = ctx->module_for(s.plan.variants[vi].name);
         if (!m->compiled) continue;
         try {
@@ -780,7 +784,7 @@ korch_status korch_profile(korch_graph* G, const int64_t* idx, int64_t n, const 
           if (r != CUDA_SUCCESS) { cu.cuEventDestroy(e0); cu.cuEventDestroy(e1); throw; }
         }
       }
-      s.best = bestv;
+      s.best = tune || keep_best < 0 ? bestv : keep_best;
       s.cost_ns = best;
       cost[k] = best;
     }

@@ -44,6 +44,11 @@ static __device__ __forceinline__ void ld_shared_bf16x8(unsigned addr, float* v)
   v[4] = __uint_as_float(c << 16); v[5] = __uint_as_float(c & 0xffff0000u);
   v[6] = __uint_as_float(d << 16); v[7] = __uint_as_float(d & 0xffff0000u);
 }
+// 8 floats from shared memory (two 16-byte loads)
+static __device__ __forceinline__ void ld_shared_f32x8(unsigned addr, float* v) {
+  asm volatile("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4];" : "=f"(v[0]), "=f"(v[1]), "=f"(v[2]), "=f"(v[3]) : "r"(addr) : "memory");
+  asm volatile("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4];" : "=f"(v[4]), "=f"(v[5]), "=f"(v[6]), "=f"(v[7]) : "r"(addr + 16u) : "memory");
+}
 static __device__ __forceinline__ void mbar_wait(unsigned long long* b, unsigned parity) {
   asm volatile(
       "{\n"

@@ -478,11 +478,10 @@ def _gemm_graph(m, k, n, batch=1, act="Relu"):
 @pytest.mark.parametrize("m,k,n,batch", [(128, 768, 768, 1), (128, 768, 2304, 1), (200, 512, 256, 2),
                                          (128, 256, 196, 1), (160, 64, 676, 1), (64, 128, 100, 1)])
 def test_every_gemm_variant(ctx, m, k, n, batch):
-    """Every launch variant (tile width, split-K with the self-cleaning scratch) of every
-    GEMM candidate; each plan executes twice and both results must match the oracle (a
-    scratch tile left dirty would double the second result).  Split-K sums partials with
-    float atomics, so the two runs may differ in the last bf16 bit: only the oracle
-    comparison is exact-tolerance, not run-to-run equality."""
+    """Every launch variant of every GEMM candidate: tile width, cluster split-K (K-slice
+    partials reduced through distributed shared memory), column-lane epilogue, residual
+    tile staged by TMA, ragged M / N / K, batch.  Each plan executes twice and both results
+    must match the oracle (state left behind by a launch would corrupt the second)."""
     c = Case(ctx, _gemm_graph(m, k, n, batch))
     for x in c.cands:
         if x["klass"] != "gemm":
