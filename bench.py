@@ -185,7 +185,7 @@ def time_plan(kg, sel, dev_in, steps=20, flush_mb=512):
 MODEL_MAX_PRIMS = 12  # SPEC S:393's default; whole models only (reading A5)
 
 
-def run_models(K, names, oracle_check=True):
+def run_models(K, names, oracle_check=True, blp_time_limit=120.0):
     """Whole paper models at their paper input sizes, bs = 1: partition,
     enumerate, compile, profile, BLP-select, then measure the chosen orchestration and the
     operator-aligned one (one kernel per unfused operator) end to end."""
@@ -214,9 +214,13 @@ def run_models(K, names, oracle_check=True):
         t1 = time.perf_counter()
         costs = kg.profile()
         t_prof = time.perf_counter() - t1
+        print(f"[models] {name}: {len(cands)} candidates, enumerate {t_enum:.0f}s, compile {t_comp:.0f}s, "
+              f"profile {t_prof:.0f}s", file=sys.stderr, flush=True)
         t1 = time.perf_counter()
-        obj, sel = kg.select(costs)
+        obj, sel = kg.select(costs, time_limit=blp_time_limit)
         t_sel = time.perf_counter() - t1
+        import paper_2406_09465_b200.select as S
+        blp_optimal = S.LAST_OPTIMAL
         base = kg.operator_aligned()
         ins = make_inputs(graph, seed=0)
         dev = K.torch_inputs(graph, {k: v[1] for k, v in ins.items()})
@@ -229,7 +233,9 @@ def run_models(K, names, oracle_check=True):
                  "latency_ms": ms_sel, "kernels": len(sel),
                  "operator_aligned_ms": ms_base, "operator_aligned_kernels": len(base),
                  "speedup_vs_operator_aligned": ms_base / ms_sel,
-                 "blp_objective_ns": obj, "operator_aligned_objective_ns": sum(costs[i] for i in base),
+                 "blp_objective_ns": obj, "blp_optimal": blp_optimal,
+                 "blp_time_limit_s_per_part": blp_time_limit,
+                 "operator_aligned_objective_ns": sum(costs[i] for i in base),
                  "compile_failures": len(kg.compile_failures),
                  "tuning_s": {"enumerate": t_enum, "compile": t_comp, "profile": t_prof, "select": t_sel}}
         kinds = {n["id"]: n["kind"] for n in kg.prim["nodes"]}
@@ -253,6 +259,7 @@ def run_models(K, names, oracle_check=True):
             entry["oracle_rel_err"] = max(errs)
             entry["oracle_s"] = time.perf_counter() - t1
         res[name] = entry
+        print("[models] " + json.dumps({name: entry}), file=sys.stderr, flush=True)
         del kg, outs, dev
         ctx.close()
         torch.cuda.empty_cache()

@@ -158,22 +158,23 @@ static int stage_pitch(int CW) { return CW + 4; }
 static int stage_bytes(int CW) { return 4 * 32 * stage_pitch(CW) * 4; }
 
 static std::string emit_tmem_epilogue(const GemmEpilogue& ep, int BN, int CW, int T, int64_t M, int64_t N,
-                                      const std::string& tmem = "tmem") {
+                                      const std::string& tmem = "tmem", const std::string& wq = "warp",
+                                      const std::string& stg_base = "smem") {
   std::ostringstream k;
   auto tmem_load = [&](const char* dst) {
     std::ostringstream t;
     if (CW <= 32) {
-      t << "      tc_ld" << CW << "(" << tmem << " + ((unsigned)(warp * 32) << 16) + (unsigned)(ch * " << CW << "), " << dst
+      t << "      tc_ld" << CW << "(" << tmem << " + ((unsigned)(" << wq << " * 32) << 16) + (unsigned)(ch * " << CW << "), " << dst
         << ");\n";
     } else {
       t << "      #pragma unroll\n      for (int q = 0; q < " << CW / 32 << "; ++q)\n"
-        << "        tc_ld32(" << tmem << " + ((unsigned)(warp * 32) << 16) + (unsigned)(ch * " << CW << " + q * 32), " << dst
+        << "        tc_ld32(" << tmem << " + ((unsigned)(" << wq << " * 32) << 16) + (unsigned)(ch * " << CW << " + q * 32), " << dst
         << " + q * 32);\n";
     }
     return t.str();
   };
   if (T == 1) {
-    k << "  {\n    const int gm = tile_m + warp * 32 + lane;\n    const int tid = 0;\n    (void)tid;\n";
+    k << "  {\n    const int gm = tile_m + " << wq << " * 32 + lane;\n    const int tid = 0;\n    (void)tid;\n";
     k << "    #pragma unroll 1\n    for (int ch = 0; ch < " << BN / CW << "; ++ch) {\n";
     k << "      const int nb = tile_n + ch * " << CW << ";\n";
     k << "      float acc[" << CW << "];\n";
@@ -184,7 +185,7 @@ static std::string emit_tmem_epilogue(const GemmEpilogue& ep, int BN, int CW, in
     return k.str();
   }
   const int P = stage_pitch(CW), R = 32 / T;
-  k << "  {\n    float* stg = reinterpret_cast<float*>(smem) + warp * " << 32 * P << ";\n";
+  k << "  {\n    float* stg = reinterpret_cast<float*>(" << stg_base << ") + " << wq << " * " << 32 * P << ";\n";
   k << "    const int tid = lane % " << T << ", rsub = lane / " << T << ";\n";
   k << "    #pragma unroll 1\n    for (int ch = 0; ch < " << BN / CW << "; ++ch) {\n";
   k << "      const int nb = tile_n + ch * " << CW << ";\n";
@@ -201,7 +202,7 @@ static std::string emit_tmem_epilogue(const GemmEpilogue& ep, int BN, int CW, in
   // masked inside the body, N % CW != 0).
   k << "      #pragma unroll\n      for (int pp = 0; pp < " << T << "; ++pp) {\n";
   k << "        const int rl = pp * " << R << " + rsub;\n";
-  k << "        const int gmr = tile_m + warp * 32 + rl;\n";
+  k << "        const int gmr = tile_m + " << wq << " * 32 + rl;\n";
   k << "        const int gm = gmr < " << M << " ? gmr : " << M - 1 << ";\n";
   k << "        float acc[8];\n";
   k << "        {\n          const float4 a0 = *reinterpret_cast<const float4*>(stg + rl * " << P << " + tid * 8);\n";
@@ -854,7 +855,7 @@ KernelPlan generate_gemm(const Graph& g, const Candidate& c) {
   //  * split-K (KS > 1) for grids far smaller than the 148 SMs: a cluster of KS CTAs
   //    accumulates the K-slices of one tile in their TMEMs and reduces them through
   //    distributed shared memory (see the KS > 1 epilogue below).
-  struct Cfg { int bn, ks; };
+  struct Cfg { int bn, ks; bool persist = false; };
   std::vector<Cfg> cfgs;
   const int64_t NKt = (K + 63) / 64;
   const int64_t Mt = (M + 127) / 128;
@@ -870,6 +871,11 @@ KernelPlan generate_gemm(const Graph& g, const Candidate& c) {
         if (NKt % ks || tiles >= 148 || tiles * ks > 2 * 148 || N % 32 || N < bn) continue;
         cfgs.push_back({bn, ks});
       }
+    // persistent tile loop with double-buffered TMEM accumulators (large grids only)
+    for (int bn : {128, 256}) {
+      const int64_t tiles = Mt * ((N + bn - 1) / bn) * batch;
+      if (tiles >= 2 * 148 && bn / 2 < N) cfgs.push_back({bn, 1, true});
+    }
   }
   bool gather_fallback = false;
   for (const Cfg& cf : cfgs) {
@@ -895,6 +901,144 @@ KernelPlan generate_gemm(const Graph& g, const Candidate& c) {
       continue;
     }
     if (!b_kmaj) db.swizzle = b_swz_tma;
+    if (cf.persist) {
+      // KB5-persistent: one CTA per SM walks the tiles t = blockIdx.x, +gridDim.x, ...
+      // warp 0 = TMA producer (ring of S stages shared by consecutive tiles), warp 1 = MMA
+      // issuer into one of two TMEM accumulators (2 x BN columns), warps 2-5 = epilogue
+      // (TMEM lane quarter = warp % 4), which drains tile i's accumulator while the MMA
+      // warp fills the other one with tile i+1: the epilogue and the next tile's operand
+      // stream overlap instead of serialising per CTA.
+      const int A_BYTES = 128 * 64 * 2, B_BYTES = BN * 64 * 2, STAGE = A_BYTES + B_BYTES;
+      const int64_t NK = NKt;
+      GemmEpilogue pe = epv;
+      const int TE = epilogue_lanes(g, c, mm, CW, pre, 1 << 30, &pe, 0);
+      const int STG = TE > 1 ? stage_bytes(CW) : 0;
+      const int S = (int)std::min<int64_t>(NK < 2 ? 2 : NK, (220 * 1024 - STG - 2048) / STAGE);
+      if (S < 2) continue;
+      const int64_t STG_OFF = (int64_t)S * STAGE, BAR_OFF = STG_OFF + STG;
+      const int smem = (int)BAR_OFF + (2 * S + 4) * 8 + 16 + 1024;
+      const int64_t Nt = (N + BN - 1) / BN, NT = Mt * Nt * batch;
+      const uint32_t idesc = (1u << 4) | (1u << 7) | (1u << 10) | ((a_kmaj ? 0u : 1u) << 15) | ((b_kmaj ? 0u : 1u) << 16) |
+                             ((uint32_t)(BN >> 3) << 17) | ((uint32_t)(128 >> 4) << 24);
+      auto coords = [&](std::string inner, std::string outer, const std::vector<int>& baxes, const View& v,
+                        bool k_inner) {
+        std::string extra;
+        if (v.ksplit) {
+          std::string& kc = k_inner ? inner : outer;
+          extra = ", (" + kc + ") / " + str(v.ksplit);
+          kc = "(" + kc + ") % " + str(v.ksplit);
+        }
+        std::string r = inner + ", " + outer + extra;
+        for (int b : baxes) r += ", " + pe.batch_vars[b];
+        return r;
+      };
+      auto load = [&](int rank) { return "tma_load_" + std::to_string(rank) + "d"; };
+      std::ostringstream decode;
+      decode << "      int tt = t;\n      const int tile_m = (tt % " << Mt << ") * 128; tt /= " << Mt << ";\n"
+             << "      const int tile_n = (tt % " << Nt << ") * " << BN << "; tt /= " << Nt << ";\n"
+             << "      int bzl = tt;\n";
+      for (int b = nbC - 1; b >= 0; --b)
+        decode << "      const int " << pe.batch_vars[b] << " = bzl % " << C[b] << "; bzl /= " << C[b] << ";\n";
+      decode << "      (void)bzl; (void)tile_m; (void)tile_n;\n";
+      std::ostringstream k;
+      k << "extern \"C\" __global__ void __launch_bounds__(192, 1) KNAME(";
+      for (size_t i = 0; i < kp.ext.size(); ++i)
+        k << "const " << (g.dtype_of(kp.ext[i]) == DType::F32 ? "float" : "bf16_t") << "* __restrict__ p" << i << ", ";
+      k << (g.prims[c.output].dtype == DType::F32 ? "float" : "bf16_t") << "* __restrict__ out, ";
+      k << "const __grid_constant__ TmaMap tmA, const __grid_constant__ TmaMap tmB) {\n";
+      k << "  typedef int idx_t;\n";
+      k << "  extern __shared__ __align__(1024) unsigned char smem_raw[];\n";
+      k << "  unsigned char* smem = (unsigned char*)(((unsigned long long)smem_raw + 1023ull) & ~1023ull);\n";
+      k << "  unsigned long long* full = (unsigned long long*)(smem + " << BAR_OFF << ");\n";
+      k << "  unsigned long long* empty = full + " << S << ";\n";
+      k << "  unsigned long long* accfull = empty + " << S << ";\n";
+      k << "  unsigned long long* accempty = accfull + 2;\n";
+      k << "  unsigned* tslot = (unsigned*)(accempty + 2);\n";
+      k << "  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;\n";
+      k << "  if (threadIdx.x == 0) {\n    for (int s = 0; s < " << S
+        << "; ++s) { mbar_init(full + s, 1); mbar_init(empty + s, 1); }\n"
+        << "    mbar_init(accfull, 1); mbar_init(accfull + 1, 1); mbar_init(accempty, 128); mbar_init(accempty + 1, 128);\n"
+        << "    mbar_fence_init();\n    tma_prefetch(&tmA);\n    tma_prefetch(&tmB);\n  }\n";
+      k << "  if (warp == 1) tc_alloc(tslot, " << 2 * BN << ");\n";
+      k << "  tc_fence_before();\n  __syncthreads();\n  tc_fence_after();\n";
+      k << "  const unsigned tmem = *tslot;\n";
+      k << "  pdl_trigger();\n  pdl_wait();\n";
+      // producer
+      k << "  if (warp == 0 && lane == 0) {\n    int s = 0; unsigned ph = 0;\n";
+      k << "    for (int t = blockIdx.x; t < " << NT << "; t += gridDim.x) {\n" << decode.str();
+      k << "      for (int kb = 0; kb < " << NK << "; ++kb) {\n";
+      k << "        mbar_wait(empty + s, ph ^ 1u);\n";
+      k << "        mbar_expect_tx(full + s, " << STAGE << "u);\n";
+      k << "        unsigned char* sa = smem + s * " << STAGE << ";\n        unsigned char* sb = sa + " << A_BYTES << ";\n";
+      if (a_kmaj) {
+        k << "        " << load(da.rank) << "(sa, &tmA, full + s, " << coords("kb * 64", "tile_m", ba_axes, va, true) << ");\n";
+      } else {
+        for (int cc = 0; cc < 2; ++cc)
+          k << "        " << load(da.rank) << "(sa + " << cc * 8192 << ", &tmA, full + s, "
+            << coords("tile_m + " + str(cc * 64), "kb * 64", ba_axes, va, false) << ");\n";
+      }
+      if (b_kmaj) {
+        k << "        " << load(db.rank) << "(sb, &tmB, full + s, " << coords("kb * 64", "tile_n", bb_axes, vb, true) << ");\n";
+      } else {
+        for (int cc = 0; cc < (BN + 63) / 64; ++cc)
+          k << "        " << load(db.rank) << "(sb + " << cc * 8192 << ", &tmB, full + s, "
+            << coords("tile_n + " + str(cc * 64), "kb * 64", bb_axes, vb, false) << ");\n";
+      }
+      k << "        if (++s == " << S << ") { s = 0; ph ^= 1u; }\n      }\n    }\n";
+      // MMA issuer
+      k << "  } else if (warp == 1 && lane == 0) {\n    int s = 0; unsigned ph = 0; int it = 0;\n";
+      k << "    for (int t = blockIdx.x; t < " << NT << "; t += gridDim.x, ++it) {\n";
+      k << "      const int buf = it & 1;\n      const unsigned use = (unsigned)(it >> 1);\n";
+      k << "      mbar_wait(accempty + buf, (use & 1u) ^ 1u);\n      tc_fence_after();\n";
+      k << "      const unsigned acc_t = tmem + (unsigned)(buf * " << BN << ");\n";
+      k << "      for (int kb = 0; kb < " << NK << "; ++kb) {\n";
+      k << "        mbar_wait(full + s, ph);\n        tc_fence_after();\n";
+      k << "        const unsigned sa = smem_u32(smem + s * " << STAGE << "), sb = sa + " << A_BYTES << ";\n";
+      k << "        #pragma unroll\n        for (int k = 0; k < 4; ++k) {\n";
+      k << "          const unsigned long long ad = umma_desc(sa + " << (a_kmaj ? "k * 32" : "k * 2048") << ", "
+        << (a_kmaj ? 16 : 8192) << ", 1024);\n";
+      if (b_kmaj)
+        k << "          const unsigned long long bd = umma_desc(sb + k * 32, 16, 1024);\n";
+      else
+        k << "          const unsigned long long bd = umma_desc(sb + k * " << 16 * b_row_bytes << ", 8192, "
+          << 8 * b_row_bytes << ", " << b_swz_umma << ");\n";
+      k << "          tc_mma(acc_t, ad, bd, " << idesc << "u, (kb | k) != 0);\n        }\n";
+      k << "        tc_commit(empty + s);\n";
+      k << "        if (++s == " << S << ") { s = 0; ph ^= 1u; }\n      }\n";
+      k << "      tc_commit(accfull + buf);\n    }\n";
+      // epilogue warps 2-5
+      k << "  } else if (warp >= 2) {\n    const int q = warp & 3;\n    int it = 0;\n";
+      k << "    for (int t = blockIdx.x; t < " << NT << "; t += gridDim.x, ++it) {\n";
+      k << "      const int buf = it & 1;\n      const unsigned use = (unsigned)(it >> 1);\n" << decode.str();
+      k << "      mbar_wait(accfull + buf, use & 1u);\n      __syncwarp();\n      tc_fence_after();\n";
+      k << "      const unsigned tmem_b = tmem + (unsigned)(buf * " << BN << ");\n";
+      k << emit_tmem_epilogue(pe, BN, CW, TE, M, N, "tmem_b", "q", "smem + " + str(STG_OFF));
+      k << "      tc_fence_before();\n      mbar_arrive(accempty + buf);\n    }\n  }\n";
+      k << "  tc_fence_before();\n  __syncthreads();\n";
+      k << "  if (warp == 1) tc_dealloc(tmem, " << 2 * BN << ");\n}\n";
+      KernelVariant kv;
+      std::string src = k.str();
+      char nm[64];
+      std::snprintf(nm, sizeof nm, "korch_gemm_%016llx",
+                    (unsigned long long)fnv1a(std::string(kSm100GemmTemplate) + "\n" + src));
+      kv.name = nm;
+      src.replace(src.find("KNAME"), 5, kv.name);
+      kv.source = src;
+      kv.tcgen05 = true;
+      kv.block = 192;
+      kv.grid = std::min<int64_t>(NT, 148);
+      kv.grid_y = 1;
+      kv.grid_z = 1;
+      kv.smem = smem;
+      kv.tma = {da, db};
+      std::ostringstream t;
+      t << "gemm-persistent BM=128 BN=" << BN << " BK=64 stages=" << S << " A=" << (a_kmaj ? "K" : "M") << "-major B="
+        << (b_kmaj ? "K" : "N") << "-major M=" << M << " N=" << N << " K=" << K << " batch=" << batch
+        << (TE > 1 ? " epi=cl" : "");
+      kv.tag = t.str();
+      kp.variants.push_back(kv);
+      continue;
+    }
     const int A_BYTES = 128 * 64 * 2, B_BYTES = BN * 64 * 2, STAGE = A_BYTES + B_BYTES;
     const int64_t NK = NKt / KS;  // K-blocks per CTA
     // Pipeline depth: keep as many K-blocks in flight as shared memory allows (up to all

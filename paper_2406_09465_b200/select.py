@@ -20,11 +20,47 @@ from scipy.sparse import coo_matrix
 INF = (1 << 63) - 1
 
 
+def prune_dominated(cands, costs, live):
+    """Exact reduction of the BLP before the MILP.
+
+    * Dominance: candidate i is dominated by j if both produce the same tensor, j reads a
+      subset of i's inputs (Eq. 4 then asks for no more materialised tensors) and
+      c_j <= c_i (ties: the lower index stays).  Swapping i for j in any feasible
+      selection keeps it feasible and neither raises the cost nor the kernel count, so an
+      optimum (with A8's tie-break) survives.
+    * Dead candidates: one that reads a tensor nobody (left) can produce can never be
+      selected under Eq. 4; removed to a fixpoint.
+    Returns the surviving candidate indices (sorted)."""
+    by_out = {}
+    for i in live:
+        by_out.setdefault(cands[i]["output"], []).append(i)
+    keep = []
+    for o, group in by_out.items():
+        group.sort(key=lambda i: (costs[i], len(cands[i]["inputs"]), i))
+        kept = []
+        for i in group:
+            ins = frozenset(cands[i]["inputs"])
+            if any(costs[j] <= costs[i] and ins_j <= ins for j, ins_j in kept):
+                continue
+            kept.append((i, ins))
+        keep.extend(i for i, _ in kept)
+    alive = set(keep)
+    changed = True
+    while changed:
+        changed = False
+        produced = {cands[i]["output"] for i in alive}
+        for i in list(alive):
+            if any(j not in produced for j in cands[i]["inputs"]):
+                alive.discard(i)
+                changed = True
+    return sorted(alive)
+
+
 def solve_blp(cands, costs, outputs, time_limit=600.0):
     """cands: list of dicts with 'output' and 'inputs'; costs: int ns (INF = rejected).
 
     Returns (objective_ns, sorted list of selected candidate indices)."""
-    live = [i for i, c in enumerate(costs) if c < INF]
+    live = prune_dominated(cands, costs, [i for i, c in enumerate(costs) if c < INF])
     idx = {i: k for k, i in enumerate(live)}
     m = len(live)
     producers = {}
@@ -50,14 +86,23 @@ def solve_blp(cands, costs, outputs, time_limit=600.0):
             lb.append(0.0)
             r += 1
     a = coo_matrix((vals, (rows, cols)), shape=(r, m)).tocsr()
-    c = np.array([float(costs[i]) * (m + 1) + 1.0 for i in live])
+    # A8 tie-break toward fewer kernels: an optimal selection has at most one producer per
+    # tensor (A7), so it has at most (#distinct outputs) kernels and a weight of that + 1
+    # per ns keeps any 1 ns difference in sum(c) above every kernel-count difference
+    w = float(len({cands[i]["output"] for i in live}) + 1)
+    c = np.array([float(costs[i]) * w + 1.0 for i in live])
     res = milp(c, integrality=np.ones(m), bounds=Bounds(0, 1),
                constraints=LinearConstraint(a, np.array(lb), np.inf),
                options={"time_limit": time_limit, "mip_rel_gap": 0.0})
     if res.x is None:
         raise RuntimeError(f"HiGHS failed: {res.message}")
+    global LAST_OPTIMAL
+    LAST_OPTIMAL = LAST_OPTIMAL and res.status == 0  # 0 = optimal; 1 = time limit (best found)
     sel = sorted(live[k] for k in range(m) if res.x[k] > 0.5)
     return int(sum(costs[i] for i in sel)), sel
+
+
+LAST_OPTIMAL = True  # False if some part of the last solve stopped at its time limit
 
 
 def solve_partitioned(cands, costs, outputs, time_limit=600.0):
@@ -66,6 +111,8 @@ def solve_partitioned(cands, costs, outputs, time_limit=600.0):
     Parts interact only through cut tensors (a part's primitives consumed by a later
     part), so the global optimum is the sum of per-part optima with
     T_part = (graph outputs in the part) + (its primitives consumed by later parts)."""
+    global LAST_OPTIMAL
+    LAST_OPTIMAL = True
     parts = sorted({c.get("part", 0) for c in cands})
     if len(parts) <= 1:
         return solve_blp(cands, costs, outputs, time_limit)

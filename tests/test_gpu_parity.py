@@ -495,6 +495,27 @@ def test_every_gemm_variant(ctx, m, k, n, batch):
 
 
 @pytest.mark.gpu
+@pytest.mark.parametrize("m,k,n,batch", [(130, 192, 520, 40), (256, 64, 1024, 24)])
+def test_persistent_gemm_every_variant(ctx, m, k, n, batch):
+    """Grids of more than two waves also get the persistent variant (one CTA per SM walking
+    the tiles, double-buffered TMEM accumulators, epilogue warps overlapping the next
+    tile's main loop); every variant of every GEMM candidate, ragged M / N, batch."""
+    c = Case(ctx, _gemm_graph(m, k, n, batch))
+    seen = 0
+    for x in c.cands:
+        if x["klass"] != "gemm":
+            continue
+        nv, _, _ = c.kg.variant_info(x["index"])
+        for v in range(nv):
+            c.kg.set_variant(x["index"], v)
+            seen += "persistent" in c.kg.variant_info(x["index"])[2]
+            sel = c.completion([x["index"]])
+            c.check(sel)
+            c.check(sel)
+    assert seen > 0
+
+
+@pytest.mark.gpu
 @pytest.mark.parametrize("m,k,n,batch", [(128, 64, 64, 1), (200, 96, 104, 1), (300, 320, 384, 2), (64, 16, 48, 3),
                                          (1024, 768, 2304, 1)])
 def test_gemm_shapes(ctx, m, k, n, batch):
