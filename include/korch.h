@@ -199,6 +199,21 @@ korch_status korch_plan(const korch_graph* g, int64_t* n_kernels, int64_t* order
 korch_status korch_execute(korch_graph* g, const void* const* inputs, void* const* outputs,
                            void* workspace, void* stream);
 
+/* End-to-end execution with host buffers (the user-facing call of an inference
+ * service: P:456-459's execution plus the transfers around it).  For every graph
+ * input i with host_inputs[i] != NULL, numel*dtype bytes are copied host -> device
+ * into dev_inputs[i] (inputs with a NULL host pointer, e.g. resident weights, are
+ * used in place); the accepted orchestration then runs exactly as in
+ * korch_execute; then every output j with host_outputs[j] != NULL is copied
+ * device -> host from dev_outputs[j].  Copies and kernels are captured into one
+ * CUDA graph per distinct pointer set and replayed asynchronously on `stream`;
+ * host buffers should be page-locked (pinned) for the copies to be asynchronous.
+ * The caller owns all buffers.  Errors: KORCH_E_ARG (no plan / NULL arrays),
+ * KORCH_E_CUDA. */
+korch_status korch_execute_host(korch_graph* g, const void* const* host_inputs,
+                                const void* const* dev_inputs, void* const* host_outputs,
+                                void* const* dev_outputs, void* workspace, void* stream);
+
 #ifdef __cplusplus
 }
 #endif

@@ -32,7 +32,7 @@ EXPORTS = [
     "korch_graph_free", "korch_graph_info", "korch_graph_dump", "korch_validate", "korch_enumerate",
     "korch_candidate", "korch_candidate_source", "korch_compile", "korch_profile",
     "korch_set_orchestration", "korch_plan", "korch_execute", "korch_variant_info", "korch_select_variant",
-    "korch_variant_cost",
+    "korch_variant_cost", "korch_execute_host",
 ]
 
 
@@ -83,6 +83,7 @@ def load():
         "korch_set_orchestration": ([P, C.POINTER(I64), I64, C.POINTER(SZ)], I32),
         "korch_plan": ([P, C.POINTER(I64), C.POINTER(I64)], I32),
         "korch_execute": ([P, C.POINTER(P), C.POINTER(P), P, P], I32),
+        "korch_execute_host": ([P, C.POINTER(P), C.POINTER(P), C.POINTER(P), C.POINTER(P), P, P], I32),
         "korch_variant_info": ([P, I64, C.POINTER(I32), C.POINTER(I32), C.c_char_p, SZ], I32),
         "korch_select_variant": ([P, I64, I32], I32),
         "korch_variant_cost": ([P, I64, I32, C.POINTER(I64)], I32),

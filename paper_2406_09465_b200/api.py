@@ -221,6 +221,22 @@ class KorchGraph:
         s = stream if isinstance(stream, int) or stream is None else stream.cuda_stream
         check(LIB.korch_execute(self.h, ia, oa, C.c_void_p(ws), C.c_void_p(s or 0)))
 
+    def execute_host(self, host_inputs, dev_inputs, host_outputs, dev_outputs, workspace, stream=None):
+        """End-to-end call (korch_execute_host): host_inputs[i] (pinned tensor / pointer, or
+        None = already resident on the device) are copied into dev_inputs[i], the plan runs,
+        and dev_outputs[j] are copied back into host_outputs[j] (None = not copied); one
+        CUDA-graph replay on `stream`."""
+        def ptr(t):
+            return 0 if t is None else t if isinstance(t, int) else t.data_ptr()
+        n_in, n_out = len(self.inputs), len(self.outputs)
+        if not (len(host_inputs) == len(dev_inputs) == n_in and len(host_outputs) == len(dev_outputs) == n_out):
+            raise ValueError("wrong number of inputs/outputs")
+        arr = lambda xs, n: (C.c_void_p * max(1, n))(*[ptr(t) for t in xs])  # noqa: E731
+        ws = ptr(workspace) if workspace is not None else 0
+        s = stream if isinstance(stream, int) or stream is None else stream.cuda_stream
+        check(LIB.korch_execute_host(self.h, arr(host_inputs, n_in), arr(dev_inputs, n_in), arr(host_outputs, n_out),
+                                     arr(dev_outputs, n_out), C.c_void_p(ws), C.c_void_p(s or 0)))
+
     # helpers for torch-resident buffers
     def torch_outputs(self, device="cuda"):
         import torch

@@ -17,7 +17,8 @@ namespace korch {
   X(cuStreamSynchronize) X(cuEventCreate) X(cuEventDestroy) X(cuEventRecord)                       \
   X(cuEventSynchronize) X(cuEventElapsedTime) X(cuStreamBeginCapture) X(cuStreamEndCapture)        \
   X(cuGraphInstantiateWithFlags) X(cuGraphLaunch) X(cuGraphExecDestroy) X(cuGraphDestroy)          \
-  X(cuGetErrorString) X(cuTensorMapEncodeTiled) X(cuMemcpyHtoD) X(cuMemcpyDtoH)
+  X(cuGetErrorString) X(cuTensorMapEncodeTiled) X(cuMemcpyHtoD) X(cuMemcpyDtoH)                 \
+  X(cuMemcpyHtoDAsync) X(cuMemcpyDtoHAsync)
 
 struct CudaApi {
 #define KORCH_DECL(name) decltype(&::name) name = nullptr;

@@ -214,6 +214,51 @@ static std::string emit_tmem_epilogue(const GemmEpilogue& ep, int BN, int CW, in
   return k.str();
 }
 
+
+// Cluster split-K reduction (KS CTAs of a cluster hold K-slice partials of one 128 x BN
+// tile in TMEM).  (1) cluster barrier: every CTA's MMAs are done, so every operand ring
+// is idle and becomes a receive buffer [KS slots][RO rows][BN (+4 pad)] fp32 at `smem`;
+// (2) each epilogue thread (warp quarter `wq`, lane = row within it) pushes its
+// accumulator row into the owner CTA of that row (rows [o*RO, (o+1)*RO) belong to rank
+// o) with st.shared::cluster; (3) cluster barrier (release/acquire); (4) the owner sums
+// the KS slots of its RO rows and runs the fused epilogue `ep` (emitted with cw = BN,
+// t = BN/8) with T = BN/8 lanes per row.  `epi_cond` selects the threads that own TMEM
+// rows (the epilogue warps); every thread of the CTA must execute this code (the cluster
+// barriers are .aligned over all threads).  No global scratch, no atomics.
+static std::string emit_dsmem_splitk(const GemmEpilogue& ep, int BN, int CW, int KS, int64_t M, int64_t N,
+                                     const std::string& epi_cond, const std::string& wq, int nthreads) {
+  std::ostringstream k;
+  const int RO = 128 / KS, PB = BN + 4, TE = BN / 8;
+  k << "  cluster_sync();\n";
+  k << "  if (" << epi_cond << ") {\n    const int r = " << wq << " * 32 + lane;\n";
+  k << "    const unsigned dst = cluster_map(smem_u32(smem) + (unsigned)((ks * " << RO << " + r % " << RO << ") * "
+    << PB * 4 << "), (unsigned)(r / " << RO << "));\n";
+  k << "    #pragma unroll 1\n    for (int ch = 0; ch < " << BN / CW << "; ++ch) {\n";
+  k << "      float accr[" << CW << "];\n";
+  k << "      tc_ld" << CW << "(tmem + ((unsigned)(" << wq << " * 32) << 16) + (unsigned)(ch * " << CW << "), accr);\n";
+  k << "      #pragma unroll\n      for (int q = 0; q < " << CW / 4 << "; ++q)\n";
+  k << "        st_cluster_v4(dst + (unsigned)((ch * " << CW << " + 4 * q) * 4), accr[4 * q], accr[4 * q + 1], "
+       "accr[4 * q + 2], accr[4 * q + 3]);\n";
+  k << "    }\n  }\n";
+  k << "  cluster_sync();\n";
+  k << "  {\n    const float* recv = reinterpret_cast<const float*>(smem);\n";
+  k << "    #pragma unroll\n    for (int it = threadIdx.x; it < " << RO * TE << "; it += " << nthreads << ") {\n";
+  k << "      const int rl = it / " << TE << ", tid = it % " << TE << ";\n";
+  k << "      const int gmr = tile_m + ks * " << RO << " + rl;\n";
+  k << "      const int gm = gmr < " << M << " ? gmr : " << M - 1 << ";\n";
+  k << "      const int nb = tile_n;\n";
+  k << "      float acc[8];\n";
+  k << "      #pragma unroll\n      for (int e = 0; e < 8; ++e) acc[e] = 0.f;\n";
+  k << "      #pragma unroll\n      for (int sl = 0; sl < " << KS << "; ++sl) {\n";
+  k << "        const float* src = recv + (sl * " << RO << " + rl) * " << PB << " + tid * 8;\n";
+  k << "        const float4 a0 = *reinterpret_cast<const float4*>(src), a1 = *reinterpret_cast<const float4*>(src + 4);\n";
+  k << "        acc[0] += a0.x; acc[1] += a0.y; acc[2] += a0.z; acc[3] += a0.w;\n";
+  k << "        acc[4] += a1.x; acc[5] += a1.y; acc[6] += a1.z; acc[7] += a1.w;\n      }\n";
+  k << "      {\n" << ep.body << "      if (gmr < " << M << ") {\n" << ep.store << "      }\n      }\n";
+  k << "    }\n  }\n";
+  return k.str();
+}
+
 // Column-lane epilogue choice: T = CW / 8 lanes per row unless the output is contiguous
 // along rows (then the row mapping already stores coalesced) or the epilogue reduces rows.
 static int epilogue_lanes(const Graph& g, const Candidate& c, int mm, int CW, const std::vector<Ref>& pre,
@@ -339,13 +384,27 @@ static KernelPlan generate_gather_gemm(const Graph& g, const Candidate& c, int m
   kp.flops = 2.0 * (double)F * (double)NP * (double)K;
   kp.bytes = ep0.bytes + 2 * F * K + gs.b_bytes;
   const int64_t NK = (K + 63) / 64, Mt = (F + 127) / 128;
-  for (int BN : {64, 128}) {
+  // launch configurations: BN in {64, 128} unsplit; cluster split-K (KS CTAs of a cluster
+  // take K-slices of NKc blocks each, the last one shorter) when the grid is small -- the
+  // gathered operand dominates these kernels, and splitting K splits the gather
+  struct GCfg { int bn, ks; };
+  std::vector<GCfg> cfgs{{64, 1}, {128, 1}};
+  for (int ks : {2, 4, 8}) {
+    const int64_t tiles = Mt * ((NP + 63) / 64), nkc = (NK + ks - 1) / ks;
+    if (tiles < 148 && tiles * ks <= 2 * 148 && (ks - 1) * nkc < NK) cfgs.push_back({64, ks});
+  }
+  for (const GCfg& cf : cfgs) {
+    const int BN = cf.bn, KS = cf.ks;
+    const int64_t NKc = (NK + KS - 1) / KS;  // K-blocks per slice (the last may be shorter)
     GemmEpilogue ep;
-    if (!make_gemm_epilogue(g, c, mm, 32, pre, &ep, &err)) continue;
+    if (!make_gemm_epilogue(g, c, mm, KS > 1 ? BN : 32, pre, &ep, &err, -1, KS > 1 ? BN / 8 : 1)) continue;
+    if (ep.ext.size() != kp.ext.size()) continue;
     const int A_BYTES = 128 * 64 * 2, B_BYTES = BN * 64 * 2, STAGE = A_BYTES + B_BYTES;
-    const int S_ = (int)std::max<int64_t>(2, std::min<int64_t>({NK, 4, (200 * 1024) / STAGE}));
-    const int smem = S_ * STAGE + 1024 + (2 * S_ + 1) * 8 + 16;
-    const int TE = epilogue_lanes(g, c, mm, 32, pre, (int64_t)S_ * STAGE, &ep);
+    const int S_ = (int)std::max<int64_t>(2, std::min<int64_t>({NKc, 4, (200 * 1024) / STAGE}));
+    const int64_t recv = KS > 1 ? (int64_t)128 * (BN + 4) * 4 : 0;
+    const int64_t REG = std::max<int64_t>((int64_t)S_ * STAGE, recv);
+    const int smem = (int)REG + 1024 + (2 * S_ + 1) * 8 + 16;
+    const int TE = KS > 1 ? BN / 8 : epilogue_lanes(g, c, mm, 32, pre, (int64_t)S_ * STAGE, &ep);
     const int64_t Nt = (NP + BN - 1) / BN;
     const int tcols = BN;
     const uint32_t idesc = (1u << 4) | (1u << 7) | (1u << 10) | (0u << 15) | (1u << 16) |
@@ -367,21 +426,27 @@ static KernelPlan generate_gather_gemm(const Graph& g, const Candidate& c, int m
     k << "  typedef int idx_t;\n";
     k << "  extern __shared__ __align__(1024) unsigned char smem_raw[];\n";
     k << "  unsigned char* smem = (unsigned char*)(((unsigned long long)smem_raw + 1023ull) & ~1023ull);\n";
-    k << "  unsigned long long* full = (unsigned long long*)(smem + " << S_ * STAGE << ");\n";
+    k << "  unsigned long long* full = (unsigned long long*)(smem + " << REG << ");\n";
     k << "  unsigned long long* empty = full + " << S_ << ";\n";
     k << "  unsigned long long* accf = empty + " << S_ << ";\n";
     k << "  unsigned* tslot = (unsigned*)(accf + 1);\n";
     k << "  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;\n";
-    k << "  const int tile_m = blockIdx.x * 128, tile_n = blockIdx.y * " << BN << ";\n";
+    if (KS > 1)
+      k << "  const int ks = blockIdx.x % " << KS << ";\n  const int tile_m = (blockIdx.x / " << KS
+        << ") * 128, tile_n = blockIdx.y * " << BN << ";\n";
+    else
+      k << "  const int ks = 0;\n  const int tile_m = blockIdx.x * 128, tile_n = blockIdx.y * " << BN << ";\n";
+    k << "  const int kb0 = ks * " << NKc << ", kb1 = kb0 + " << NKc << " < " << NK << " ? kb0 + " << NKc << " : " << NK
+      << ";\n";
     k << "  if (threadIdx.x == 0) {\n    for (int s = 0; s < " << S_
       << "; ++s) { mbar_init(full + s, 5); mbar_init(empty + s, 1); }\n"
       << "    mbar_init(accf, 1);\n    mbar_fence_init();\n    tma_prefetch(&tmA);\n";
     // weights (a graph input): first PRE stages fetched before the programmatic-dependency wait
-    const int64_t PRE = gs.a_src.is_input ? std::min<int64_t>(S_, NK) : 0;
-    if (PRE) {
-      k << "    for (int s = 0; s < " << PRE << "; ++s) {\n";
+    const bool early = gs.a_src.is_input;
+    if (early) {
+      k << "    for (int s = 0; s < " << S_ << " && kb0 + s < kb1; ++s) {\n";
       k << "      mbar_expect_tx(full + s, " << A_BYTES << "u);\n";
-      k << "      tma_load_2d(smem + s * " << STAGE << ", &tmA, full + s, s * 64, tile_m);\n    }\n";
+      k << "      tma_load_2d(smem + s * " << STAGE << ", &tmA, full + s, (kb0 + s) * 64, tile_m);\n    }\n";
     }
     k << "  }\n";
     k << "  if (warp == 5) tc_alloc(tslot, " << tcols << ");\n";
@@ -392,7 +457,7 @@ static KernelPlan generate_gather_gemm(const Graph& g, const Candidate& c, int m
     k << "  if (warp < 4) {\n";
     k << "    const bf16_t* __restrict__ xin = p" << slotX << ";\n";
     k << "    int s = 0; unsigned ph = 0;\n";
-    k << "    for (int kb = 0; kb < " << NK << "; ++kb) {\n";
+    k << "    for (int kb = kb0; kb < kb1; ++kb) {\n";
     k << "      mbar_wait(empty + s, ph ^ 1u);\n";
     k << "      const unsigned sb = smem_u32(smem + s * " << STAGE << " + " << A_BYTES << ");\n";
     k << "      for (int u = threadIdx.x; u < " << 64 * (BN / 8) << "; u += 128) {\n";
@@ -417,30 +482,35 @@ static KernelPlan generate_gather_gemm(const Graph& g, const Candidate& c, int m
     // weight TMA: warp 4
     k << "  } else if (warp == 4 && lane == 0) {\n";
     k << "    int s = 0; unsigned ph = 0;\n";
-    k << "    for (int kb = 0; kb < " << NK << "; ++kb) {\n";
+    k << "    for (int kb = kb0; kb < kb1; ++kb) {\n";
     k << "      mbar_wait(empty + s, ph ^ 1u);\n";
-    k << "      if (kb >= " << PRE << ") {\n";
+    k << "      if (" << (early ? "kb - kb0 >= " + str(S_) : std::string("true")) << ") {\n";
     k << "      mbar_expect_tx(full + s, " << A_BYTES << "u);\n";
     k << "      tma_load_2d(smem + s * " << STAGE << ", &tmA, full + s, kb * 64, tile_m);\n      }\n";
     k << "      if (++s == " << S_ << ") { s = 0; ph ^= 1u; }\n    }\n";
     // MMA: warp 5
     k << "  } else if (warp == 5 && lane == 0) {\n";
     k << "    int s = 0; unsigned ph = 0;\n";
-    k << "    for (int kb = 0; kb < " << NK << "; ++kb) {\n";
+    k << "    for (int kb = kb0; kb < kb1; ++kb) {\n";
     k << "      mbar_wait(full + s, ph);\n      tc_fence_after();\n";
     k << "      const unsigned sa = smem_u32(smem + s * " << STAGE << "), sb = sa + " << A_BYTES << ";\n";
     k << "      #pragma unroll\n      for (int k = 0; k < 4; ++k) {\n";
     k << "        const unsigned long long ad = umma_desc(sa + k * 32, 16, 1024);\n";
     k << "        const unsigned long long bd = umma_desc(sb + k * 2048, 8192, 1024);\n";
-    k << "        tc_mma(tmem, ad, bd, " << idesc << "u, (kb | k) != 0);\n      }\n";
+    k << "        tc_mma(tmem, ad, bd, " << idesc << "u, kb != kb0 || k != 0);\n      }\n";
     k << "      tc_commit(empty + s);\n";
     k << "      if (++s == " << S_ << ") { s = 0; ph ^= 1u; }\n    }\n";
     k << "    tc_commit(accf);\n  }\n";
     // epilogue: warps 0-3 (TMEM lane quarters 0-3)
     k << "  __syncwarp();\n";
-    k << "  if (warp < 4) {\n    mbar_wait(accf, 0);\n    __syncwarp();\n    tc_fence_after();\n";
-    k << emit_tmem_epilogue(ep, BN, 32, TE, F, NP);
-    k << "  }\n";
+    if (KS == 1) {
+      k << "  if (warp < 4) {\n    mbar_wait(accf, 0);\n    __syncwarp();\n    tc_fence_after();\n";
+      k << emit_tmem_epilogue(ep, BN, 32, TE, F, NP);
+      k << "  }\n";
+    } else {
+      k << "  if (warp < 4) {\n    mbar_wait(accf, 0);\n    __syncwarp();\n    tc_fence_after();\n  }\n";
+      k << emit_dsmem_splitk(ep, BN, 32, KS, F, NP, "warp < 4", "warp", 192);
+    }
     k << "  tc_fence_before();\n  __syncthreads();\n";
     k << "  if (warp == 5) tc_dealloc(tmem, " << tcols << ");\n}\n";
 
@@ -455,13 +525,14 @@ static KernelPlan generate_gather_gemm(const Graph& g, const Candidate& c, int m
     kv.source = src;
     kv.tcgen05 = true;
     kv.block = 192;
-    kv.grid = Mt;
+    kv.grid = Mt * KS;
     kv.grid_y = Nt;
     kv.grid_z = 1;
+    kv.cluster = KS;
     kv.smem = smem;
     kv.tma = {da};
     std::ostringstream t;
-    t << gs.tag << " BM=128 BN=" << BN << " BK=64 stages=" << S_ << (TE > 1 ? " epi=cl" : "");
+    t << gs.tag << " BM=128 BN=" << BN << " BK=64 splitK=" << KS << " stages=" << S_ << (TE > 1 ? " epi=cl" : "");
     kv.tag = t.str();
     kp.variants.push_back(kv);
   }
@@ -1252,41 +1323,7 @@ KernelPlan generate_gemm(const Graph& g, const Candidate& c) {
       }
       k << emit_tmem_epilogue(ep, BN, CW, TE, M, N);
     } else {
-      // Cluster split-K: the KS CTAs of a cluster hold K-slice partials of one tile in
-      // TMEM.  (1) cluster barrier: every CTA's MMAs are done, so every operand ring is
-      // idle and becomes a receive buffer [KS slots][RO rows][BN (+4 pad)] fp32;
-      // (2) each thread pushes its accumulator row into the owner CTA of that row
-      // (rows [o*RO, (o+1)*RO) belong to rank o) with st.shared::cluster; (3) cluster
-      // barrier (release/acquire); (4) each CTA sums the KS slots of its RO rows and runs
-      // the fused epilogue, T = BN/8 lanes per row (coalesced side reads and stores).
-      // No global scratch, no atomics, nothing to re-zero.
-      k << "  cluster_sync();\n";
-      k << "  {\n    const int r = warp * 32 + lane;\n";
-      k << "    const unsigned dst = cluster_map(smem_u32(smem) + (unsigned)((ks * " << RO << " + r % " << RO << ") * "
-        << PB * 4 << "), (unsigned)(r / " << RO << "));\n";
-      k << "    #pragma unroll 1\n    for (int ch = 0; ch < " << BN / CW << "; ++ch) {\n";
-      k << "      float accr[" << CW << "];\n";
-      k << "      tc_ld" << CW << "(tmem + ((unsigned)(warp * 32) << 16) + (unsigned)(ch * " << CW << "), accr);\n";
-      k << "      #pragma unroll\n      for (int q = 0; q < " << CW / 4 << "; ++q)\n";
-      k << "        st_cluster_v4(dst + (unsigned)((ch * " << CW << " + 4 * q) * 4), accr[4 * q], accr[4 * q + 1], "
-           "accr[4 * q + 2], accr[4 * q + 3]);\n";
-      k << "    }\n  }\n";
-      k << "  cluster_sync();\n";
-      k << "  {\n    const float* recv = reinterpret_cast<const float*>(smem);\n";
-      k << "    #pragma unroll\n    for (int it = threadIdx.x; it < " << RO * TE << "; it += 128) {\n";
-      k << "      const int rl = it / " << TE << ", tid = it % " << TE << ";\n";
-      k << "      const int gmr = tile_m + ks * " << RO << " + rl;\n";
-      k << "      const int gm = gmr < " << M << " ? gmr : " << M - 1 << ";\n";
-      k << "      const int nb = tile_n;\n";
-      k << "      float acc[8];\n";
-      k << "      #pragma unroll\n      for (int e = 0; e < 8; ++e) acc[e] = 0.f;\n";
-      k << "      #pragma unroll\n      for (int sl = 0; sl < " << KS << "; ++sl) {\n";
-      k << "        const float* src = recv + (sl * " << RO << " + rl) * " << PB << " + tid * 8;\n";
-      k << "        const float4 a0 = *reinterpret_cast<const float4*>(src), a1 = *reinterpret_cast<const float4*>(src + 4);\n";
-      k << "        acc[0] += a0.x; acc[1] += a0.y; acc[2] += a0.z; acc[3] += a0.w;\n";
-      k << "        acc[4] += a1.x; acc[5] += a1.y; acc[6] += a1.z; acc[7] += a1.w;\n      }\n";
-      k << "      {\n" << ep.body << "      if (gmr < " << M << ") {\n" << ep.store << "      }\n      }\n";
-      k << "    }\n  }\n";
+      k << emit_dsmem_splitk(ep, BN, CW, KS, M, N, "true", "warp", 128);
     }
     k << "  tc_fence_before();\n  __syncthreads();\n";
     k << "  if (warp == 2) tc_dealloc(tmem, " << tcols << ");\n}\n";

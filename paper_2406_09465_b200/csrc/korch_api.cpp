@@ -134,11 +134,12 @@ struct korch_graph {
   std::vector<Step> steps;
   size_t ws_bytes = 0;
   // captured executable
-  std::vector<const void*> cap_ptrs;
-  CUgraphExec gexec = nullptr;
+  std::vector<const void*> cap_ptrs, cap_ptrs_host;
+  CUgraphExec gexec = nullptr, gexec_host = nullptr;  // korch_execute / korch_execute_host
   std::mutex mu;
   ~korch_graph() {
     if (gexec && cuda().ok) cuda().cuGraphExecDestroy(gexec);
+    if (gexec_host && cuda().ok) cuda().cuGraphExecDestroy(gexec_host);
   }
 };
 
@@ -936,7 +937,9 @@ korch_status korch_set_orchestration(korch_graph* G, const int64_t* sel, int64_t
     G->ws_bytes = top;
     G->has_plan = true;
     if (G->gexec && cuda().ok) { cuda().cuGraphExecDestroy(G->gexec); G->gexec = nullptr; }
+    if (G->gexec_host && cuda().ok) { cuda().cuGraphExecDestroy(G->gexec_host); G->gexec_host = nullptr; }
     G->cap_ptrs.clear();
+    G->cap_ptrs_host.clear();
     if (ws) *ws = top;
     return KORCH_OK;
   })
@@ -1006,6 +1009,63 @@ korch_status korch_execute(korch_graph* G, const void* const* inputs, void* cons
       G->cap_ptrs = ptrs;
     }
     CU_CHECK(cu.cuGraphLaunch(G->gexec, (CUstream)stream));
+    return KORCH_OK;
+  })
+}
+
+korch_status korch_execute_host(korch_graph* G, const void* const* host_inputs, const void* const* dev_inputs,
+                                void* const* host_outputs, void* const* dev_outputs, void* workspace, void* stream) {
+  if (!G) return fail(KORCH_E_ARG, "NULL graph");
+  if (!host_inputs || !dev_inputs || !host_outputs || !dev_outputs) return fail(KORCH_E_ARG, "NULL pointer array");
+  if (!G->has_plan) return fail(KORCH_E_ARG, "no accepted orchestration (call korch_set_orchestration)");
+  KORCH_TRY({
+    korch_ctx* ctx = G->ctx;
+    ctx->bind();
+    CudaApi& cu = cuda();
+    std::lock_guard<std::mutex> lk(G->mu);
+    const Graph& g = G->g;
+    std::vector<const void*> ptrs;
+    for (size_t i = 0; i < g.inputs.size(); ++i) { ptrs.push_back(host_inputs[i]); ptrs.push_back(dev_inputs[i]); }
+    for (size_t i = 0; i < g.outputs.size(); ++i) { ptrs.push_back(host_outputs[i]); ptrs.push_back(dev_outputs[i]); }
+    ptrs.push_back(workspace);
+    auto resolve = [&](const BufRef& b) -> void* {
+      if (b.kind == BufRef::Input) return const_cast<void*>(dev_inputs[b.index]);
+      if (b.kind == BufRef::Output) return dev_outputs[b.index];
+      return static_cast<char*>(workspace) + b.offset;
+    };
+    static const bool use_pdl = !(getenv("KORCH_PDL") && std::string(getenv("KORCH_PDL")) == "0");
+    if (!G->gexec_host || ptrs != G->cap_ptrs_host) {
+      for (auto& st : G->steps) prepare_variant(ctx, G->cs[st.cand].plan.variants[st.variant]);
+      if (G->gexec_host) { cu.cuGraphExecDestroy(G->gexec_host); G->gexec_host = nullptr; }
+      CU_CHECK(cu.cuStreamBeginCapture(ctx->pstream, CU_STREAM_CAPTURE_MODE_THREAD_LOCAL));
+      try {
+        for (size_t i = 0; i < g.inputs.size(); ++i)
+          if (host_inputs[i])
+            CU_CHECK(cu.cuMemcpyHtoDAsync((CUdeviceptr)dev_inputs[i], host_inputs[i],
+                                          (size_t)tensor_bytes(g, Ref{true, (int)i}), ctx->pstream));
+        for (size_t k = 0; k < G->steps.size(); ++k) {
+          const Step& st = G->steps[k];
+          std::vector<const void*> ins;
+          for (auto& a : st.args) ins.push_back(resolve(a));
+          launch_variant(ctx, G->cs[st.cand].plan, st.variant, ins, resolve(st.out), ctx->pstream, use_pdl && k > 0);
+        }
+        for (size_t j = 0; j < g.outputs.size(); ++j)
+          if (host_outputs[j])
+            CU_CHECK(cu.cuMemcpyDtoHAsync(host_outputs[j], (CUdeviceptr)dev_outputs[j],
+                                          (size_t)tensor_bytes(g, Ref{false, g.outputs[j]}), ctx->pstream));
+      } catch (...) {
+        CUgraph tmp = nullptr;
+        cu.cuStreamEndCapture(ctx->pstream, &tmp);
+        if (tmp) cu.cuGraphDestroy(tmp);
+        throw;
+      }
+      CUgraph graph;
+      CU_CHECK(cu.cuStreamEndCapture(ctx->pstream, &graph));
+      CU_CHECK(cu.cuGraphInstantiateWithFlags(&G->gexec_host, graph, 0));
+      cu.cuGraphDestroy(graph);
+      G->cap_ptrs_host = ptrs;
+    }
+    CU_CHECK(cu.cuGraphLaunch(G->gexec_host, (CUstream)stream));
     return KORCH_OK;
   })
 }

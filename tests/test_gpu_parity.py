@@ -460,6 +460,36 @@ def test_c2_pipeline(ctx, kw):
     c.check(c.kg.singletons())
 
 
+@pytest.mark.gpu
+def test_execute_host_matches_execute(ctx):
+    """korch_execute_host (H2D of the activation, the plan, D2H of the output in one graph
+    replay) gives bitwise the same output as korch_execute on device buffers; repeated
+    with a second input to check the copies are replayed, not cached."""
+    import torch
+    c = Case(ctx, c2_vit_attention())
+    costs = c.kg.profile()
+    _, sel = c.kg.select(costs)
+    c.kg.set_orchestration(sel)
+    ws = c.kg.torch_workspace()
+    names = [s["name"] for s in c.graph["inputs"]]
+    xi = names.index("x")
+    for trial in range(2):
+        x_host = (c.dev_in[xi].float() * (1 + trial)).to(c.dev_in[xi].dtype).cpu().pin_memory()
+        dev = list(c.dev_in)
+        dev[xi] = torch.empty_like(c.dev_in[xi])
+        hin = [x_host if i == xi else None for i in range(len(names))]
+        outs = c.kg.torch_outputs()
+        host_out = [torch.empty_like(o, device="cpu").pin_memory() for o in outs]
+        c.kg.execute_host(hin, dev, host_out, outs, ws, torch.cuda.current_stream())
+        torch.cuda.synchronize()
+        ref_in = list(c.dev_in)
+        ref_in[xi] = x_host.cuda()
+        ref = c.kg.torch_outputs()
+        c.kg.execute(ref_in, ref, ws, torch.cuda.current_stream())
+        torch.cuda.synchronize()
+        assert torch.equal(host_out[0], ref[0].cpu())
+
+
 def _gemm_graph(m, k, n, batch=1, act="Relu"):
     b = GraphBuilder("bf16")
     x = b.input("x", [batch, m, k])

@@ -168,6 +168,24 @@ def test_blp_matches_exact_search_c1(ctx):
         kg.set_orchestration(sel)          # the library accepts it (Eq. 3/4)
 
 
+def test_blp_pruning_exact_on_random_graphs(ctx):
+    """The BLP's exact reductions (dominance, dead candidates) keep the optimum: random
+    operator DAGs, costs drawn from 3 values (many ties, the hard case for dominance),
+    objective == the oracle's producer-assignment search, selection feasible."""
+    rng = np.random.default_rng(11)
+    for _ in range(20):
+        g = _random_op_graph(rng, int(rng.integers(2, 7)))
+        kg = KorchGraph(ctx, g)
+        cands = kg.enumerate(max_prims=8)
+        G, ref = _oracle_cands(g, max_prims=8)
+        cin = [candidate_inputs(G, m) for m, _ in ref]
+        costs = [int(rng.integers(1, 4)) * 1000 for _ in cands]
+        obj, sel = solve_blp(cands, costs, kg.outputs)
+        best, _ = producer_search(ref, costs, G.pg["outputs"], cin, G.topo_index)
+        assert obj == best
+        assert feasible(ref, sel, G.pg["outputs"], cin)
+
+
 @pytest.mark.parametrize("name,pm", [("c2", 8), ("c2", 12), ("c2_r1r3", 10), ("misc", 6), ("c1", 5)])
 def test_partitioned_enumeration_matches_oracle(ctx, name, pm):
     from oracle.enumeration import candidates_partitioned, partition
