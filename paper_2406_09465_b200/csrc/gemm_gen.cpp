@@ -137,6 +137,10 @@ struct GatherSpec {
   int64_t a_off = 0, a_row = 0;   // A = [M, K] K-major view: element offset, row stride (elements)
   std::string elem;               // per-element gather code
   std::string prologue;           // per-k code shared by the 8 elements of a group
+  // optional vector path: code defining `vok` (the group's 8 elements are 8 consecutive
+  // in-bounds bf16 of the source) and `vidx` (index of the first); the group is then read
+  // with two aligned 16-byte loads and a funnel shift instead of 8 scalar loads
+  std::string vec;
   std::string tag;
   std::string prefix;             // kernel name prefix
   int64_t b_bytes = 0;            // algorithmic bytes of B
@@ -320,6 +324,19 @@ static KernelPlan generate_conv_gemm(const Graph& g, const Candidate& c, int mm)
   el << "          const size_t idx = (((size_t)img * " << Cin << " + ci) * " << H << " + ih) * " << W << " + iw;\n";
   gs.prologue = pr.str();
   gs.elem = el.str();
+  if (L.stride[1] == 1 && OW % 8 == 0) {
+    // stride-1 rows: 8 consecutive output pixels (never straddling a row since OW % 8 == 0
+    // and groups start at multiples of 8) read 8 consecutive input elements of one row
+    std::ostringstream ve;
+    ve << "        const int p0 = tile_n + grp * 8;\n";
+    ve << "        const int img0 = p0 / " << OH * OW << ", q0 = p0 % " << OH * OW << ";\n";
+    ve << "        const int ih0 = (q0 / " << OW << ") * " << L.stride[0] << " + rr - " << L.cpad[0] << ";\n";
+    ve << "        const int iw0 = (q0 % " << OW << ") + ss - " << L.cpad[1] << ";\n";
+    ve << "        const bool vok = kg < " << K << " && p0 + 7 < " << NP << " && (unsigned)ih0 < " << H
+       << "u && iw0 >= 0 && iw0 + 7 < " << W << ";\n";
+    ve << "        const size_t vidx = (((size_t)img0 * " << Cin << " + ci) * " << H << " + ih0) * " << W << " + iw0;\n";
+    gs.vec = ve.str();
+  }
   std::ostringstream t;
   t << "conv-igemm F=" << F << " P=" << NP << " K=" << K << " (" << R << "x" << S << " s" << L.stride[0] << ")";
   gs.tag = t.str();
@@ -464,15 +481,22 @@ static KernelPlan generate_gather_gemm(const Graph& g, const Candidate& c, int m
     k << "        const int kk = u / " << BN / 8 << ", grp = u % " << BN / 8 << ";\n";
     k << "        const int kg = kb * 64 + kk;\n";
     k << gs.prologue;
+    k << "        uint4 pk;\n";
+    if (!gs.vec.empty()) {
+      k << gs.vec;
+      k << "        if (vok) {\n          pk = ld_bf16x8_unaligned(xin + vidx);\n        } else {\n";
+    } else {
+      k << "        {\n";
+    }
     k << "        unsigned short v[8];\n";
     k << "        #pragma unroll\n        for (int e = 0; e < 8; ++e) {\n";
     k << "          const int p = tile_n + grp * 8 + e;\n";
     k << gs.elem;
     k << "          v[e] = ok ? __ldg(xin + idx) : (unsigned short)0;\n";
     k << "        }\n";
-    k << "        uint4 pk;\n";
     k << "        pk.x = v[0] | ((unsigned)v[1] << 16); pk.y = v[2] | ((unsigned)v[3] << 16);\n";
     k << "        pk.z = v[4] | ((unsigned)v[5] << 16); pk.w = v[6] | ((unsigned)v[7] << 16);\n";
+    k << "        }\n";
     // MN-major SW128 canonical: 64-pixel atoms 8 KB apart, K rows 128 B, 16B chunk ^ (row % 8)
     k << "        st_shared_v4(sb + (grp >> 3) * 8192 + kk * 128 + (((grp & 7) ^ (kk & 7)) << 4), pk);\n";
     k << "      }\n";

@@ -1013,6 +1013,63 @@ korch_status korch_execute(korch_graph* G, const void* const* inputs, void* cons
   })
 }
 
+// Host <-> device transfers of korch_execute_host as a kernel: page-locked host memory is
+// mapped into the device's unified address space, so 16-byte loads/stores over the
+// host link replace copy-engine memcpy nodes (whose per-copy set-up dominates at the
+// ~100 KB sizes of a bs-1 inference).  Falls back to memcpy nodes when a buffer is not
+// device-accessible or not 16-byte aligned.
+static const KernelVariant& copy_variant() {
+  static KernelVariant v = [] {
+    KernelVariant k;
+    k.name = "korch_copy16_v1";
+    k.block = 256;
+    k.source =
+        "extern \"C\" __global__ void __launch_bounds__(256) korch_copy16_v1(const uint4* __restrict__ src, "
+        "uint4* __restrict__ dst, unsigned long long n16) {\n"
+        "  pdl_trigger();\n  pdl_wait();\n"
+        "  for (unsigned long long i = blockIdx.x * 256ull + threadIdx.x; i < n16; i += gridDim.x * 256ull)\n"
+        "    dst[i] = src[i];\n}\n";
+    return k;
+  }();
+  return v;
+}
+
+static bool launch_copy(korch_ctx* ctx, const void* src, void* dst, size_t bytes, CUstream stream, bool pdl) {
+  CudaApi& cu = cuda();
+  if (((unsigned long long)src | (unsigned long long)dst | bytes) & 15) return false;
+  CUdeviceptr ds = 0, dd = 0;
+  if (cu.cuPointerGetAttribute(&ds, CU_POINTER_ATTRIBUTE_DEVICE_POINTER, (CUdeviceptr)src) != CUDA_SUCCESS) return false;
+  if (cu.cuPointerGetAttribute(&dd, CU_POINTER_ATTRIBUTE_DEVICE_POINTER, (CUdeviceptr)dst) != CUDA_SUCCESS) return false;
+  const KernelVariant& v = copy_variant();
+  Module* m = ctx->module_for(v.name);
+  if (!m->compiled || !m->fn) return false;  // prepare_copy() runs before stream capture
+  CUfunction fn = m->fn;
+  unsigned long long n16 = bytes / 16;
+  unsigned grid = (unsigned)std::max<unsigned long long>(1, std::min<unsigned long long>(4 * 148, (n16 + 255) / 256));
+  void* args[] = {&ds, &dd, &n16};
+  CUlaunchConfig cfg{};
+  cfg.gridDimX = grid;
+  cfg.gridDimY = cfg.gridDimZ = 1;
+  cfg.blockDimX = 256;
+  cfg.blockDimY = cfg.blockDimZ = 1;
+  cfg.hStream = stream;
+  CUlaunchAttribute at[1];
+  at[0].id = CU_LAUNCH_ATTRIBUTE_PROGRAMMATIC_STREAM_SERIALIZATION;
+  at[0].value.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = pdl ? 1 : 0;
+  CU_CHECK(cu.cuLaunchKernelEx(&cfg, fn, args, nullptr));
+  return true;
+}
+
+// compile (cached) and load the copy kernel; must run outside stream capture
+static void prepare_copy(korch_ctx* ctx) {
+  const KernelVariant& v = copy_variant();
+  Module* m = ctx->module_for(v.name);
+  if (!m->compiled && !m->failed) compile_batch({{m, &v}}, default_cache_dir());
+  if (m->compiled) load_fn(ctx, m, v);
+}
+
 korch_status korch_execute_host(korch_graph* G, const void* const* host_inputs, const void* const* dev_inputs,
                                 void* const* host_outputs, void* const* dev_outputs, void* workspace, void* stream) {
   if (!G) return fail(KORCH_E_ARG, "NULL graph");
@@ -1036,23 +1093,32 @@ korch_status korch_execute_host(korch_graph* G, const void* const* host_inputs, 
     static const bool use_pdl = !(getenv("KORCH_PDL") && std::string(getenv("KORCH_PDL")) == "0");
     if (!G->gexec_host || ptrs != G->cap_ptrs_host) {
       for (auto& st : G->steps) prepare_variant(ctx, G->cs[st.cand].plan.variants[st.variant]);
+      prepare_copy(ctx);
       if (G->gexec_host) { cu.cuGraphExecDestroy(G->gexec_host); G->gexec_host = nullptr; }
       CU_CHECK(cu.cuStreamBeginCapture(ctx->pstream, CU_STREAM_CAPTURE_MODE_THREAD_LOCAL));
       try {
+        static const bool ce_only = getenv("KORCH_E2E_MEMCPY") != nullptr;
+        bool any = false;
         for (size_t i = 0; i < g.inputs.size(); ++i)
-          if (host_inputs[i])
-            CU_CHECK(cu.cuMemcpyHtoDAsync((CUdeviceptr)dev_inputs[i], host_inputs[i],
-                                          (size_t)tensor_bytes(g, Ref{true, (int)i}), ctx->pstream));
+          if (host_inputs[i]) {
+            const size_t nb = (size_t)tensor_bytes(g, Ref{true, (int)i});
+            if (ce_only || !launch_copy(ctx, host_inputs[i], const_cast<void*>(dev_inputs[i]), nb, ctx->pstream,
+                                        use_pdl && any))
+              CU_CHECK(cu.cuMemcpyHtoDAsync((CUdeviceptr)dev_inputs[i], host_inputs[i], nb, ctx->pstream));
+            any = true;
+          }
         for (size_t k = 0; k < G->steps.size(); ++k) {
           const Step& st = G->steps[k];
           std::vector<const void*> ins;
           for (auto& a : st.args) ins.push_back(resolve(a));
-          launch_variant(ctx, G->cs[st.cand].plan, st.variant, ins, resolve(st.out), ctx->pstream, use_pdl && k > 0);
+          launch_variant(ctx, G->cs[st.cand].plan, st.variant, ins, resolve(st.out), ctx->pstream, use_pdl && (k > 0 || any));
         }
         for (size_t j = 0; j < g.outputs.size(); ++j)
-          if (host_outputs[j])
-            CU_CHECK(cu.cuMemcpyDtoHAsync(host_outputs[j], (CUdeviceptr)dev_outputs[j],
-                                          (size_t)tensor_bytes(g, Ref{false, g.outputs[j]}), ctx->pstream));
+          if (host_outputs[j]) {
+            const size_t nb = (size_t)tensor_bytes(g, Ref{false, g.outputs[j]});
+            if (ce_only || !launch_copy(ctx, dev_outputs[j], host_outputs[j], nb, ctx->pstream, use_pdl))
+              CU_CHECK(cu.cuMemcpyDtoHAsync(host_outputs[j], (CUdeviceptr)dev_outputs[j], nb, ctx->pstream));
+          }
       } catch (...) {
         CUgraph tmp = nullptr;
         cu.cuStreamEndCapture(ctx->pstream, &tmp);

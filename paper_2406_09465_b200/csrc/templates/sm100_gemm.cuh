@@ -173,6 +173,32 @@ static __device__ __forceinline__ bool elect_one() {
   return pred != 0;
 }
 
+// 8 consecutive bf16 at a 2-byte-aligned global address: two aligned 16-byte read-only
+// loads and a funnel shift (the second load only when the window straddles 16 bytes;
+// it stays inside the 16-byte block holding the last requested element)
+static __device__ __forceinline__ uint4 ld_bf16x8_unaligned(const unsigned short* p) {
+  const unsigned long long a = (unsigned long long)p;
+  const uint4* q = reinterpret_cast<const uint4*>(a & ~15ull);
+  const unsigned off = (unsigned)(a & 15ull);
+  const uint4 lo = __ldg(q);
+  if (off == 0) return lo;
+  const uint4 hi = __ldg(q + 1);
+  const unsigned sh = (off & 3u) * 8u;
+  unsigned w0, w1, w2, w3, w4;
+  switch (off >> 2) {
+    case 0: w0 = lo.x; w1 = lo.y; w2 = lo.z; w3 = lo.w; w4 = hi.x; break;
+    case 1: w0 = lo.y; w1 = lo.z; w2 = lo.w; w3 = hi.x; w4 = hi.y; break;
+    case 2: w0 = lo.z; w1 = lo.w; w2 = hi.x; w3 = hi.y; w4 = hi.z; break;
+    default: w0 = lo.w; w1 = hi.x; w2 = hi.y; w3 = hi.z; w4 = hi.w; break;
+  }
+  uint4 r;
+  r.x = __funnelshift_r(w0, w1, sh);
+  r.y = __funnelshift_r(w1, w2, sh);
+  r.z = __funnelshift_r(w2, w3, sh);
+  r.w = __funnelshift_r(w3, w4, sh);
+  return r;
+}
+
 // ---------------------------------------------------------------- clusters / DSMEM
 // full cluster barrier (all threads of every CTA; release/acquire orders DSMEM traffic)
 static __device__ __forceinline__ void cluster_sync() {

@@ -96,13 +96,16 @@ def solve_blp(cands, costs, outputs, time_limit=600.0):
                options={"time_limit": time_limit, "mip_rel_gap": 0.0})
     if res.x is None:
         raise RuntimeError(f"HiGHS failed: {res.message}")
-    global LAST_OPTIMAL
+    global LAST_OPTIMAL, LAST_GAP
     LAST_OPTIMAL = LAST_OPTIMAL and res.status == 0  # 0 = optimal; 1 = time limit (best found)
+    gap = getattr(res, "mip_gap", 0.0)
+    LAST_GAP = max(LAST_GAP, float(gap) if gap is not None and res.status != 0 else 0.0)
     sel = sorted(live[k] for k in range(m) if res.x[k] > 0.5)
     return int(sum(costs[i] for i in sel)), sel
 
 
 LAST_OPTIMAL = True  # False if some part of the last solve stopped at its time limit
+LAST_GAP = 0.0       # largest relative MIP gap left by a time-limited part
 
 
 def solve_partitioned(cands, costs, outputs, time_limit=600.0):
@@ -111,8 +114,8 @@ def solve_partitioned(cands, costs, outputs, time_limit=600.0):
     Parts interact only through cut tensors (a part's primitives consumed by a later
     part), so the global optimum is the sum of per-part optima with
     T_part = (graph outputs in the part) + (its primitives consumed by later parts)."""
-    global LAST_OPTIMAL
-    LAST_OPTIMAL = True
+    global LAST_OPTIMAL, LAST_GAP
+    LAST_OPTIMAL, LAST_GAP = True, 0.0
     parts = sorted({c.get("part", 0) for c in cands})
     if len(parts) <= 1:
         return solve_blp(cands, costs, outputs, time_limit)

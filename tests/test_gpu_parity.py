@@ -384,11 +384,14 @@ def _conv_graph(n, c, h, w, f, k, s, p):
 
 @pytest.mark.gpu
 @pytest.mark.parametrize("shape", [(1, 16, 20, 24, 32, 3, 1, 1), (1, 32, 17, 19, 48, 3, 2, 1), (2, 64, 14, 14, 160, 1, 1, 0),
-                                   (1, 128, 28, 28, 128, 3, 1, 1), (1, 32, 30, 30, 64, 5, 2, 2)])
+                                   (1, 128, 28, 28, 128, 3, 1, 1), (1, 32, 30, 30, 64, 5, 2, 2),
+                                   (1, 32, 16, 32, 3, 9, 1, 4), (2, 16, 8, 16, 48, 5, 1, 2)])
 def test_conv_igemm_every_variant(ctx, shape):
     """tcgen05 implicit-GEMM convolution (KB6): every launch variant of every conv
     candidate (conv alone, + bias, + bias + ReLU), strides, zero padding, filter / pixel
-    tails, batch > 1."""
+    tails, batch > 1, cluster split-K, and the 16-byte unaligned row reads of stride-1
+    convolutions with OW % 8 == 0 (9x9 / 5x5 windows: groups at the padded edges fall
+    back to element loads)."""
     c = Case(ctx, _conv_graph(*shape))
     convs = [x for x in c.cands if x["klass"] == "gemm"]
     assert convs, "conv candidates must be accepted by the implicit-GEMM template"
