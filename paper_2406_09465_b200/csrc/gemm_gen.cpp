@@ -404,8 +404,10 @@ static KernelPlan generate_gather_gemm(const Graph& g, const Candidate& c, int m
   // launch configurations: BN in {64, 128} unsplit; cluster split-K (KS CTAs of a cluster
   // take K-slices of NKc blocks each, the last one shorter) when the grid is small -- the
   // gathered operand dominates these kernels, and splitting K splits the gather
-  struct GCfg { int bn, ks; };
-  std::vector<GCfg> cfgs{{64, 1}, {128, 1}};
+  // occupancy variant: a 2-stage ring (~50 KB of shared memory) lets several CTAs share an
+  // SM, so more gather warps hide the scattered-load latency
+  struct GCfg { int bn, ks, stages = 0; };
+  std::vector<GCfg> cfgs{{64, 1}, {128, 1}, {64, 1, 2}};
   for (int ks : {2, 4, 8}) {
     const int64_t tiles = Mt * ((NP + 63) / 64), nkc = (NK + ks - 1) / ks;
     if (tiles < 148 && tiles * ks <= 2 * 148 && (ks - 1) * nkc < NK) cfgs.push_back({64, ks});
@@ -417,7 +419,8 @@ static KernelPlan generate_gather_gemm(const Graph& g, const Candidate& c, int m
     if (!make_gemm_epilogue(g, c, mm, KS > 1 ? BN : 32, pre, &ep, &err, -1, KS > 1 ? BN / 8 : 1)) continue;
     if (ep.ext.size() != kp.ext.size()) continue;
     const int A_BYTES = 128 * 64 * 2, B_BYTES = BN * 64 * 2, STAGE = A_BYTES + B_BYTES;
-    const int S_ = (int)std::max<int64_t>(2, std::min<int64_t>({NKc, 4, (200 * 1024) / STAGE}));
+    const int S_ = cf.stages ? cf.stages : (int)std::max<int64_t>(2, std::min<int64_t>({NKc, 4, (200 * 1024) / STAGE}));
+    if (cf.stages && NKc <= cf.stages) continue;  // identical to the default ring
     const int64_t recv = KS > 1 ? (int64_t)128 * (BN + 4) * 4 : 0;
     const int64_t REG = std::max<int64_t>((int64_t)S_ * STAGE, recv);
     const int smem = (int)REG + 1024 + (2 * S_ + 1) * 8 + 16;
