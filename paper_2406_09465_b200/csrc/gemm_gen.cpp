@@ -158,6 +158,13 @@ struct GatherSpec {
 //    reads and of the store covers 32/T rows of 8T contiguous columns instead of 32 rows
 //    of 16 bytes.  The staging buffer aliases the operand ring, which is idle once the
 //    accumulator barrier has fired (every TMA load was consumed by an MMA before it).
+// tcgen05.alloc takes a power of two >= 32 columns (BN = 160 for an in-tile row
+// reduction over N = 160 allocates 256)
+static int tmem_cols(int n) {
+  int c = 32;
+  while (c < n) c <<= 1;
+  return c;
+}
 static int stage_pitch(int CW) { return CW + 4; }
 static int stage_bytes(int CW) { return 4 * 32 * stage_pitch(CW) * 4; }
 
@@ -426,7 +433,7 @@ static KernelPlan generate_gather_gemm(const Graph& g, const Candidate& c, int m
     const int smem = (int)REG + 1024 + (2 * S_ + 1) * 8 + 16;
     const int TE = KS > 1 ? BN / 8 : epilogue_lanes(g, c, mm, 32, pre, (int64_t)S_ * STAGE, &ep);
     const int64_t Nt = (NP + BN - 1) / BN;
-    const int tcols = BN;
+    const int tcols = tmem_cols(BN);
     const uint32_t idesc = (1u << 4) | (1u << 7) | (1u << 10) | (0u << 15) | (1u << 16) |
                            ((uint32_t)(BN >> 3) << 17) | ((uint32_t)(128 >> 4) << 24);
     TmaDesc da;
@@ -624,7 +631,7 @@ static KernelPlan generate_prologue_gemm(const Graph& g, const Candidate& c, int
     if (S < std::min<int64_t>(2, NKA)) { kp.reject = "prologue GEMM: shared memory"; continue; }
     const int smem = A_RES + S * B_BYTES + 1024 + (2 * S + 3) * 8 + 16;
     const int TE = epilogue_lanes(g, c, mm, CW, pro.ext, (int64_t)A_RES + (int64_t)S * B_BYTES, &ep);
-    const int tcols = BN < 32 ? 32 : BN;
+    const int tcols = tmem_cols(BN);
     const int64_t Mt = (M + 127) / 128, Nt = (N + BN - 1) / BN;
     const int bmn_box = BN < 64 ? BN : 64;
     const int b_swz_tma = bmn_box == 64 ? 3 : bmn_box == 32 ? 2 : 1;
@@ -1209,7 +1216,7 @@ KernelPlan generate_gemm(const Graph& g, const Candidate& c) {
     if (!side_ok) continue;
     if (REG + 1024 + (2 * S + 2) * 8 + 16 > 227 * 1024) continue;
     const int smem = (int)REG + 1024 + (2 * S + 2) * 8 + 16;
-    const int tcols = BN < 32 ? 32 : BN;
+    const int tcols = tmem_cols(BN);
     const int64_t Nt = (N + BN - 1) / BN;
     uint32_t idesc = (1u << 4) | (1u << 7) | (1u << 10) | ((a_kmaj ? 0u : 1u) << 15) | ((b_kmaj ? 0u : 1u) << 16) |
                      ((uint32_t)(BN >> 3) << 17) | ((uint32_t)(128 >> 4) << 24);

@@ -464,6 +464,29 @@ def test_c2_pipeline(ctx, kw):
 
 
 @pytest.mark.gpu
+@pytest.mark.parametrize("n", [160, 96])
+def test_gemm_in_tile_layernorm_non_pow2_width(ctx, n):
+    """GEMM whose epilogue reduces whole rows (Linear -> LayerNorm over N): one tile spans
+    the row, TMEM allocation rounded up to a power of two (N = 160 -> 256 columns)."""
+    b = GraphBuilder("bf16")
+    x = b.input("x", [1, 200, 64])
+    w = b.input("w", [64, n], std=0.125)
+    bias = b.input("bias", [n], std=0.1)
+    g_ = b.input("g", [n], mean=1.0, std=0.1)
+    be = b.input("be", [n], std=0.1)
+    y = b.op("Add", b.op("MatMul", x, w), bias)
+    b.output(b.op("LayerNorm", y, g_, be, axis=-1, eps=1e-6))
+    c = Case(ctx, b.build())
+    gem = [x["index"] for x in c.cands if x["klass"] == "gemm" and len(x["members"]) >= 6]
+    assert gem
+    for i in gem:
+        nv, _, _ = c.kg.variant_info(i)
+        for v in range(nv):
+            c.kg.set_variant(i, v)
+            c.check(c.completion([i]))
+
+
+@pytest.mark.gpu
 def test_execute_host_matches_execute(ctx):
     """korch_execute_host (H2D of the activation, the plan, D2H of the output in one graph
     replay) gives bitwise the same output as korch_execute on device buffers; repeated
