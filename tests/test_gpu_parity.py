@@ -328,6 +328,30 @@ def test_misc_memory_bound_ops(ctx):
     c.check(c.kg.operator_aligned())
 
 
+@pytest.mark.gpu
+@pytest.mark.parametrize("shape", [(1, 32, 20, 24, 32, 3, 1, 32), (1, 3, 16, 40, 16, 3, 1, 1), (2, 12, 9, 33, 8, 5, 2, 1),
+                                   (1, 16, 8, 64, 16, 7, 3, 16)])
+def test_simt_conv_row_vector_reads(ctx, shape):
+    """SIMT convolutions (depthwise / few channels per group) with stride 1 along W read a
+    thread's 8-output window row with one unaligned 16-byte load (interior) or guarded
+    element loads (edges, ragged row tail): every generable candidate against the oracle."""
+    n, c_, h, w, f, k, p, groups = shape
+    b = GraphBuilder("bf16")
+    x = b.input("x", [n, c_, h, w])
+    wt = b.input("w", [f, c_ // groups, k, k], std=0.3)
+    bias = b.input("bias", [f], std=0.1)
+    y = b.op("Conv", x, wt, bias, stride=[1, 1], pads=[p, p], groups=groups)
+    b.output(b.op("SiLU", y))
+    c = Case(ctx, b.build())
+    gen = [x["index"] for x in c.cands if x["klass"] != "rejected"]
+    assert gen
+    for i in gen:
+        nv, _, _ = c.kg.variant_info(i)
+        for v in range(nv):
+            c.kg.set_variant(i, v)
+            c.check(c.completion([i]))
+
+
 def _cnn_graph(dtype="bf16"):
     b = GraphBuilder(dtype)
     x = b.input("x", [1, 16, 20, 24])
