@@ -1144,7 +1144,9 @@ KernelPlan generate_gemm(const Graph& g, const Candidate& c) {
       kp.variants.push_back(kv);
       continue;
     }
-    const int A_BYTES = 128 * 64 * 2, B_BYTES = BN * 64 * 2, STAGE = A_BYTES + B_BYTES;
+    // an MN-major B tile arrives as 64-column TMA boxes: BN = 96 / 160 / 224 (in-tile row
+    // reductions over N) occupy ceil(BN / 64) whole boxes in shared memory
+    const int A_BYTES = 128 * 64 * 2, B_BYTES = (b_kmaj || BN < 64 ? BN : (BN + 63) / 64 * 64) * 64 * 2, STAGE = A_BYTES + B_BYTES;
     const int64_t NK = NKt / KS;  // K-blocks per CTA
     // Pipeline depth: keep as many K-blocks in flight as shared memory allows (up to all
     // of them) -- small-M GEMMs are bound by TMA round-trip latency, not bandwidth.
