@@ -511,6 +511,47 @@ def test_gemm_in_tile_layernorm_non_pow2_width(ctx, n):
 
 
 @pytest.mark.gpu
+def test_c2_batch64_bench_plan(ctx):
+    """The bench's scaled workload at full size (C2, batch 64, M = 8192): profile, BLP,
+    execute, whole output against the oracle (persistent / wide-tile GEMM variants are
+    eligible at this size)."""
+    c = Case(ctx, c2_vit_attention(batch=64))
+    costs = c.kg.profile()
+    _, sel = c.kg.select(costs)
+    c.check(sel)
+
+
+@pytest.mark.gpu
+def test_c1_bandwidth_variant_sampled_rows(ctx):
+    """The C1 bandwidth variant at its bench size (x[2^20, 128] fp32, 512 MiB in and out):
+    the BLP-selected plan on the GPU, 4096 sampled rows checked against the oracle (rows
+    are independent in softmax -> LayerNorm, so the oracle evaluates only those rows)."""
+    import torch
+    from paper_2406_09465_b200 import KorchGraph, torch_inputs
+    rows = 1 << 20
+    g = c1_softmax_layernorm(rows=rows)
+    kg = KorchGraph(ctx, g)
+    kg.enumerate()
+    costs = kg.profile()
+    _, sel = kg.select(costs)
+    kg.set_orchestration(sel)
+    ins = make_inputs(g, seed=0)
+    dev = torch_inputs(g, {k: v[1] for k, v in ins.items()})
+    outs, ws = kg.torch_outputs(), kg.torch_workspace()
+    kg.execute(dev, outs, ws, torch.cuda.current_stream())
+    torch.cuda.synchronize()
+    pick = np.sort(np.random.default_rng(5).choice(rows, 4096, replace=False))
+    got = outs[0][torch.as_tensor(pick, device=outs[0].device)].cpu().numpy().astype(np.float64)
+    gs = c1_softmax_layernorm(rows=len(pick))
+    vals = {k: v[0] for k, v in ins.items()}
+    vals["x"] = vals["x"][pick]
+    pg = fission(gs)
+    want = eval_primitive_graph(pg, vals)[pg["outputs"][0]]
+    err = np.max(np.abs(got - want)) / np.max(np.abs(want))
+    assert err <= RTOL["f32"], err
+
+
+@pytest.mark.gpu
 def test_execute_host_matches_execute(ctx):
     """korch_execute_host (H2D of the activation, the plan, D2H of the output in one graph
     replay) gives bitwise the same output as korch_execute on device buffers; repeated
