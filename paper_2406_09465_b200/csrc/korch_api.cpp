@@ -192,13 +192,29 @@ static std::shared_ptr<const std::string> read_file_cached(const std::string& pa
   return p;
 }
 
+static void write_atomic(const std::string& path, const std::string& data);
+
+// KORCH_CACHE_FALLBACK: a read-only older cache; kernels found there are copied into the
+// current cache (batch cubin + ref), so rebuilding a cache keeps only live kernels
+// without recompiling them
 static bool cache_lookup(Module* m, const KernelVariant& v, const std::string& cache_dir) {
   if (cache_dir.empty()) return false;
-  std::ifstream ref(cache_dir + "/" + v.name + ".ref");
-  if (!ref) return false;
-  std::string batch;
-  std::getline(ref, batch);
-  auto bytes = read_file_cached(cache_dir + "/" + batch);
+  auto from = [&](const std::string& dir) -> std::shared_ptr<const std::string> {
+    std::ifstream ref(dir + "/" + v.name + ".ref");
+    if (!ref) return nullptr;
+    std::string batch;
+    std::getline(ref, batch);
+    auto bytes = read_file_cached(dir + "/" + batch);
+    if (bytes && dir != cache_dir) {
+      std::ifstream have(cache_dir + "/" + batch);
+      if (!have) write_atomic(cache_dir + "/" + batch, *bytes);
+      write_atomic(cache_dir + "/" + v.name + ".ref", batch + "\n");
+    }
+    return bytes;
+  };
+  auto bytes = from(cache_dir);
+  const char* fb = getenv("KORCH_CACHE_FALLBACK");
+  if (!bytes && fb && *fb) bytes = from(fb);
   if (!bytes) return false;
   m->cubin = bytes;
   m->compiled = true;
