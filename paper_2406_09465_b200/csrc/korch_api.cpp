@@ -769,12 +769,14 @@ korch_status korch_profile(korch_graph* G, const int64_t* idx, int64_t n, const 
             // Cold-L2 timing: the flush, two event-record nodes and the kernel form one
             // graph, so the events bracket the kernel on the device with no host launch
             // latency in between.
+            // (event records inside a capture must be EXTERNAL to become timestamped
+            // event-record nodes instead of capture-internal dependencies)
             if (flush) {
               CU_CHECK(cu.cuMemsetD8Async(ctx->flush, 0x5a, ctx->flush_bytes, ctx->pstream));
-              CU_CHECK(cu.cuEventRecord(e0, ctx->pstream));
+              CU_CHECK(cu.cuEventRecordWithFlags(e0, ctx->pstream, CU_EVENT_RECORD_EXTERNAL));
             }
             for (int l = 0; l < nl; ++l) launch_variant(ctx, s.plan, vi, ins, outp, ctx->pstream, l > 0);
-            if (flush) CU_CHECK(cu.cuEventRecord(e1, ctx->pstream));
+            if (flush) CU_CHECK(cu.cuEventRecordWithFlags(e1, ctx->pstream, CU_EVENT_RECORD_EXTERNAL));
           } catch (...) {
             CUgraph tmp;
             cu.cuStreamEndCapture(ctx->pstream, &tmp);

@@ -552,6 +552,22 @@ def test_c1_bandwidth_variant_sampled_rows(ctx):
 
 
 @pytest.mark.gpu
+def test_cold_l2_profile_is_finite(ctx):
+    """Cold-L2 re-timing (flush + event-record nodes + kernel in one graph) returns a finite
+    cost for the chosen variant and leaves the variant choice unchanged."""
+    from paper_2406_09465_b200 import INF, KorchGraph
+    kg = KorchGraph(ctx, c2_vit_attention())
+    cands = kg.enumerate(attention_pairs=True)
+    gem = [c["index"] for c in cands if c["klass"] == "gemm"][:3]
+    warm = kg.profile(gem)
+    chosen = [kg.variant_info(i)[1] for i in gem]
+    cold = kg.profile(gem, flush_l2=True, tune=False)
+    assert all(0 < c < INF for c in cold), cold
+    assert [kg.variant_info(i)[1] for i in gem] == chosen
+    assert all(c >= 0.5 * w for c, w in zip(cold, warm))
+
+
+@pytest.mark.gpu
 def test_execute_host_matches_execute(ctx):
     """korch_execute_host (H2D of the activation, the plan, D2H of the output in one graph
     replay) gives bitwise the same output as korch_execute on device buffers; repeated
