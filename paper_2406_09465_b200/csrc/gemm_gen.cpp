@@ -1,7 +1,8 @@
 // KB5: GEMM template for candidates with exactly one dense linear primitive (MatMul /
 // batched MatMul), the paper's "compute-intensive" class, re-designed for
 // sm_100a: tcgen05.mma (bf16 in, fp32 accumulate in TMEM), operands staged by TMA into a
-// 4-stage mbarrier ring with 128B swizzle, one 128 x BN tile per CTA.
+// multi-stage mbarrier ring with 128B swizzle, one 128 x BN tile per CTA (or a persistent
+// tile loop, see the persistent variant).
 //
 // Upstream members (Transpose / Reshape / Slice chains feeding the MatMul) are folded
 // into the TMA tensor maps as strided views -- the data-layout trick of P:529-531
