@@ -676,8 +676,9 @@ def main():
             "latency_ms_rank0": dist_ms,
             "plan_roofline": plan_roof,
             "e2e": {"value": e2e_max, "unit": "ms", "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
-                    "call": "korch_execute_host (pinned host buffers; copy kernels over mapped memory + plan in one "
-                            "graph replay; weights resident)"},
+                    "call": "korch_execute_host (pinned host buffers; H2D copy kernel over mapped memory, plan, "
+                            "output written by its kernel straight into mapped host memory; one graph replay; "
+                            "weights resident)"},
             "gpu_launches": len(order) * args.steps,
             "kernels_per_step": len(order),
             "selection": {"blp_objective_ns": obj, "operator_aligned_ns": base_obj,

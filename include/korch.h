@@ -205,7 +205,9 @@ korch_status korch_execute(korch_graph* g, const void* const* inputs, void* cons
  * into dev_inputs[i] (inputs with a NULL host pointer, e.g. resident weights, are
  * used in place); the accepted orchestration then runs exactly as in
  * korch_execute; then every output j with host_outputs[j] != NULL is copied
- * device -> host from dev_outputs[j].  Copies and kernels are captured into one
+ * device -> host from dev_outputs[j] -- or, when host_outputs[j] is page-locked,
+ * mapped and 16-byte aligned, written there directly by the kernel producing it
+ * (dev_outputs[j] is then left untouched).  Copies and kernels are captured into one
  * CUDA graph per distinct pointer set and replayed asynchronously on `stream`;
  * host buffers should be page-locked (pinned) for the copies to be asynchronous.
  * The caller owns all buffers.  Errors: KORCH_E_ARG (no plan / NULL arrays),

@@ -1116,9 +1116,21 @@ korch_status korch_execute_host(korch_graph* G, const void* const* host_inputs, 
     for (size_t i = 0; i < g.inputs.size(); ++i) { ptrs.push_back(host_inputs[i]); ptrs.push_back(dev_inputs[i]); }
     for (size_t i = 0; i < g.outputs.size(); ++i) { ptrs.push_back(host_outputs[i]); ptrs.push_back(dev_outputs[i]); }
     ptrs.push_back(workspace);
+    // Outputs whose host buffer is mapped into the device's address space (page-locked,
+    // 16-byte aligned) are written by their producing kernel straight into host memory:
+    // no device output buffer, no D2H copy.
+    static const bool ce_only = getenv("KORCH_E2E_MEMCPY") != nullptr;
+    std::vector<void*> direct_out(g.outputs.size(), nullptr);
+    for (size_t j = 0; j < g.outputs.size(); ++j) {
+      CUdeviceptr d = 0;
+      if (!ce_only && host_outputs[j] && ((unsigned long long)host_outputs[j] & 15) == 0 &&
+          cu.cuPointerGetAttribute(&d, CU_POINTER_ATTRIBUTE_DEVICE_POINTER, (CUdeviceptr)host_outputs[j]) ==
+              CUDA_SUCCESS)
+        direct_out[j] = (void*)d;
+    }
     auto resolve = [&](const BufRef& b) -> void* {
       if (b.kind == BufRef::Input) return const_cast<void*>(dev_inputs[b.index]);
-      if (b.kind == BufRef::Output) return dev_outputs[b.index];
+      if (b.kind == BufRef::Output) return direct_out[b.index] ? direct_out[b.index] : dev_outputs[b.index];
       return static_cast<char*>(workspace) + b.offset;
     };
     static const bool use_pdl = !(getenv("KORCH_PDL") && std::string(getenv("KORCH_PDL")) == "0");
@@ -1128,7 +1140,6 @@ korch_status korch_execute_host(korch_graph* G, const void* const* host_inputs, 
       if (G->gexec_host) { cu.cuGraphExecDestroy(G->gexec_host); G->gexec_host = nullptr; }
       CU_CHECK(cu.cuStreamBeginCapture(ctx->pstream, CU_STREAM_CAPTURE_MODE_THREAD_LOCAL));
       try {
-        static const bool ce_only = getenv("KORCH_E2E_MEMCPY") != nullptr;
         bool any = false;
         for (size_t i = 0; i < g.inputs.size(); ++i)
           if (host_inputs[i]) {
@@ -1145,7 +1156,7 @@ korch_status korch_execute_host(korch_graph* G, const void* const* host_inputs, 
           launch_variant(ctx, G->cs[st.cand].plan, st.variant, ins, resolve(st.out), ctx->pstream, use_pdl && (k > 0 || any));
         }
         for (size_t j = 0; j < g.outputs.size(); ++j)
-          if (host_outputs[j]) {
+          if (host_outputs[j] && !direct_out[j]) {
             const size_t nb = (size_t)tensor_bytes(g, Ref{false, g.outputs[j]});
             if (ce_only || !launch_copy(ctx, dev_outputs[j], host_outputs[j], nb, ctx->pstream, use_pdl))
               CU_CHECK(cu.cuMemcpyDtoHAsync(host_outputs[j], (CUdeviceptr)dev_outputs[j], nb, ctx->pstream));
