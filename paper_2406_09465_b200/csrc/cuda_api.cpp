@@ -55,6 +55,7 @@ NvrtcApi& nvrtc() {
     KORCH_LOADN(nvrtcGetCUBINSize)
     KORCH_LOADN(nvrtcGetCUBIN)
     KORCH_LOADN(nvrtcGetErrorString)
+    KORCH_LOADN(nvrtcVersion)
 #undef KORCH_LOADN
     api.ok = true;
   });

@@ -37,6 +37,7 @@ struct NvrtcApi {
   decltype(&::nvrtcGetCUBINSize) nvrtcGetCUBINSize = nullptr;
   decltype(&::nvrtcGetCUBIN) nvrtcGetCUBIN = nullptr;
   decltype(&::nvrtcGetErrorString) nvrtcGetErrorString = nullptr;
+  decltype(&::nvrtcVersion) nvrtcVersion = nullptr;
   bool ok = false;
   std::string err;
 };

@@ -1,6 +1,7 @@
 // C ABI (include/korch.h): graph load, enumeration, kernel generation/compilation,
 // on-device profiling (PROFILING) and the executor.
 #include <algorithm>
+#include <array>
 #include <atomic>
 #include <chrono>
 #include <cmath>
@@ -72,6 +73,7 @@ struct korch_ctx {
   CUdeviceptr flush = 0;
   size_t flush_bytes = 0;
   std::mutex mu;
+  std::mutex capture_mu;                // stream captures on pstream (execute, execute_host, profile)
   std::map<std::string, std::unique_ptr<Module>> modules;  // kernel name -> module
   std::map<const std::string*, CUmodule> loaded;           // batch cubin -> loaded module
   std::map<std::string, int64_t> timings;                  // kernel + protocol -> ns
@@ -169,6 +171,30 @@ static std::string full_source(const KernelVariant& v) {
   return kernel_prelude() + (v.tcgen05 ? std::string(kSm100GemmTemplate) + "\n" : std::string()) + v.source;
 }
 
+// NVRTC options of every kernel compile; part of the cache key
+static const char* const kNvrtcOpts[] = {"-arch=sm_100a", "-std=c++17", "-default-device", "-lineinfo", "-DNDEBUG",
+                                         "--diag-suppress=177,550"};
+
+// Kernel names hash only the generated body (plus the GEMM template for tcgen05 kernels).
+// Everything else that goes into the cubin -- the shared prelude, the template, the NVRTC
+// options and the NVRTC version -- salts the cache key, so a change to any of them misses
+// the on-disk cache instead of loading a stale cubin.
+static std::string cache_key(const KernelVariant& v) {
+  static const std::array<std::string, 2> salt = [] {
+    std::string opts;
+    for (const char* o : kNvrtcOpts) opts += std::string(o) + " ";
+    int maj = 0, mnr = 0;
+    if (nvrtc().ok && nvrtc().nvrtcVersion) nvrtc().nvrtcVersion(&maj, &mnr);
+    opts += "nvrtc" + std::to_string(maj) + "." + std::to_string(mnr);
+    char a[24], b[24];
+    std::snprintf(a, sizeof a, "%016llx", (unsigned long long)fnv1a(kernel_prelude() + opts));
+    std::snprintf(b, sizeof b, "%016llx",
+                  (unsigned long long)fnv1a(kernel_prelude() + std::string(kSm100GemmTemplate) + opts));
+    return std::array<std::string, 2>{a, b};
+  }();
+  return v.name + "." + salt[v.tcgen05 ? 1 : 0];
+}
+
 // Batched NVRTC compilation: up to kBatch kernels per program, so the per-program
 // overhead (front-end start-up, prelude and template parsing) is paid once per batch.
 // The batch cubin is shared by its kernels; the on-disk cache keeps one file per batch
@@ -200,7 +226,7 @@ static void write_atomic(const std::string& path, const std::string& data);
 static bool cache_lookup(Module* m, const KernelVariant& v, const std::string& cache_dir) {
   if (cache_dir.empty()) return false;
   auto from = [&](const std::string& dir) -> std::shared_ptr<const std::string> {
-    std::ifstream ref(dir + "/" + v.name + ".ref");
+    std::ifstream ref(dir + "/" + cache_key(v) + ".ref");
     if (!ref) return nullptr;
     std::string batch;
     std::getline(ref, batch);
@@ -208,7 +234,7 @@ static bool cache_lookup(Module* m, const KernelVariant& v, const std::string& c
     if (bytes && dir != cache_dir) {
       std::ifstream have(cache_dir + "/" + batch);
       if (!have) write_atomic(cache_dir + "/" + batch, *bytes);
-      write_atomic(cache_dir + "/" + v.name + ".ref", batch + "\n");
+      write_atomic(cache_dir + "/" + cache_key(v) + ".ref", batch + "\n");
     }
     return bytes;
   };
@@ -232,8 +258,8 @@ static bool nvrtc_compile(const std::string& src, const std::string& name, std::
     *log = "nvrtcCreateProgram failed";
     return false;
   }
-  const char* opts[] = {"-arch=sm_100a", "-std=c++17", "-default-device", "-lineinfo", "-DNDEBUG", "--diag-suppress=177,550"};
-  nvrtcResult r = nv.nvrtcCompileProgram(prog, 6, opts);
+  nvrtcResult r = nv.nvrtcCompileProgram(prog, (int)(sizeof kNvrtcOpts / sizeof kNvrtcOpts[0]),
+                                         const_cast<const char**>(kNvrtcOpts));
   size_t ls = 0;
   nv.nvrtcGetProgramLogSize(prog, &ls);
   std::string lg(ls, '\0');
@@ -279,7 +305,7 @@ static void compile_batch(const std::vector<std::pair<Module*, const KernelVaria
     auto shared = std::make_shared<const std::string>(std::move(cubin));
     if (!cache_dir.empty()) {
       write_atomic(cache_dir + "/" + bname, *shared);
-      for (auto& j : jobs) write_atomic(cache_dir + "/" + j.second->name + ".ref", std::string(bname) + "\n");
+      for (auto& j : jobs) write_atomic(cache_dir + "/" + cache_key(*j.second) + ".ref", std::string(bname) + "\n");
     }
     for (auto& j : jobs) {
       std::lock_guard<std::mutex> lk(j.first->mu);
@@ -762,6 +788,7 @@ korch_status korch_profile(korch_graph* G, const int64_t* idx, int64_t n, const 
             if (!flush && ms > 0.005f) nl = std::max(1, std::min(nl, (int)(0.1f / ms)));
             if (ms > 0.2f) ntr = std::min(ntr, 3);
           }
+          std::lock_guard<std::mutex> cap(ctx->capture_mu);
           CU_CHECK(cu.cuStreamBeginCapture(ctx->pstream, CU_STREAM_CAPTURE_MODE_THREAD_LOCAL));
           try {
             // launches after the first use programmatic dependent launch, as the executor
@@ -1018,6 +1045,7 @@ korch_status korch_execute(korch_graph* G, const void* const* inputs, void* cons
     }
     if (!G->gexec || ptrs != G->cap_ptrs) {
       if (G->gexec) { cu.cuGraphExecDestroy(G->gexec); G->gexec = nullptr; }
+      std::lock_guard<std::mutex> cap(ctx->capture_mu);
       CU_CHECK(cu.cuStreamBeginCapture(ctx->pstream, CU_STREAM_CAPTURE_MODE_THREAD_LOCAL));
       try {
         for (size_t k = 0; k < G->steps.size(); ++k) {
@@ -1121,9 +1149,15 @@ korch_status korch_execute_host(korch_graph* G, const void* const* host_inputs, 
     // no device output buffer, no D2H copy.
     static const bool ce_only = getenv("KORCH_E2E_MEMCPY") != nullptr;
     std::vector<void*> direct_out(g.outputs.size(), nullptr);
+    // ... unless a kernel of the plan also reads that output (its consumers would then
+    // read, or build TMA maps over, system memory across the host link)
+    std::vector<bool> read_in_plan(g.outputs.size(), false);
+    for (auto& st : G->steps)
+      for (auto& a : st.args)
+        if (a.kind == BufRef::Output) read_in_plan[a.index] = true;
     for (size_t j = 0; j < g.outputs.size(); ++j) {
       CUdeviceptr d = 0;
-      if (!ce_only && host_outputs[j] && ((unsigned long long)host_outputs[j] & 15) == 0 &&
+      if (!ce_only && !read_in_plan[j] && host_outputs[j] && ((unsigned long long)host_outputs[j] & 15) == 0 &&
           cu.cuPointerGetAttribute(&d, CU_POINTER_ATTRIBUTE_DEVICE_POINTER, (CUdeviceptr)host_outputs[j]) ==
               CUDA_SUCCESS)
         direct_out[j] = (void*)d;
@@ -1138,9 +1172,10 @@ korch_status korch_execute_host(korch_graph* G, const void* const* host_inputs, 
       for (auto& st : G->steps) prepare_variant(ctx, G->cs[st.cand].plan.variants[st.variant]);
       prepare_copy(ctx);
       if (G->gexec_host) { cu.cuGraphExecDestroy(G->gexec_host); G->gexec_host = nullptr; }
+      std::lock_guard<std::mutex> cap(ctx->capture_mu);
       CU_CHECK(cu.cuStreamBeginCapture(ctx->pstream, CU_STREAM_CAPTURE_MODE_THREAD_LOCAL));
       try {
-        bool any = false;
+        bool any = false;  // a copy kernel was launched before this one (PDL between copies)
         for (size_t i = 0; i < g.inputs.size(); ++i)
           if (host_inputs[i]) {
             const size_t nb = (size_t)tensor_bytes(g, Ref{true, (int)i});
@@ -1153,7 +1188,11 @@ korch_status korch_execute_host(korch_graph* G, const void* const* host_inputs, 
           const Step& st = G->steps[k];
           std::vector<const void*> ins;
           for (auto& a : st.args) ins.push_back(resolve(a));
-          launch_variant(ctx, G->cs[st.cand].plan, st.variant, ins, resolve(st.out), ctx->pstream, use_pdl && (k > 0 || any));
+          // the first plan kernel is launched WITHOUT programmatic serialisation: plan
+          // kernels fetch graph inputs (weights, residual tiles, a staged LayerNorm input)
+          // before griddepcontrol.wait, and here the inputs are being written by the copy
+          // kernels just launched, so the plan may only start once they have completed
+          launch_variant(ctx, G->cs[st.cand].plan, st.variant, ins, resolve(st.out), ctx->pstream, use_pdl && k > 0);
         }
         for (size_t j = 0; j < g.outputs.size(); ++j)
           if (host_outputs[j] && !direct_out[j]) {

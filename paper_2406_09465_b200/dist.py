@@ -51,7 +51,11 @@ def merge_costs(local_idx, local_costs, local_variants, n_items, device=None):
     keys = torch.full((n_items,), INF, dtype=torch.int64, device=device)
     for i, c, v in zip(local_idx, local_costs, local_variants):
         if c < INF:
-            keys[i] = (int(c) << 8) | (int(max(v, 0)) & 0xFF)
+            if not 0 <= int(max(v, 0)) < 256:
+                raise ValueError(f"candidate {i}: launch variant {v} does not fit the 8-bit key field")
+            if int(c) >= 1 << 54:
+                raise ValueError(f"candidate {i}: cost {c} ns does not fit the cost field")
+            keys[i] = (int(c) << 8) | int(max(v, 0))
     if dist.is_available() and dist.is_initialized():
         dist.all_reduce(keys, op=dist.ReduceOp.MIN)
     costs, variants = [], []

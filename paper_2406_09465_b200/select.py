@@ -13,11 +13,91 @@ c_i*(M+1) + 1 breaks ties toward fewer kernels (reading A8).
 """
 from __future__ import annotations
 
+import ctypes as C
+import os
+
 import numpy as np
 from scipy.optimize import Bounds, LinearConstraint, milp
 from scipy.sparse import coo_matrix
 
 INF = (1 << 63) - 1
+
+_SEL_LIB = None
+
+
+def _select_lib():
+    """libkorch_select.so (include/korch_select.h), built in-tree by build.py."""
+    global _SEL_LIB
+    if _SEL_LIB is None:
+        path = os.path.join(os.path.dirname(os.path.abspath(__file__)), "libkorch_select.so")
+        lib = C.CDLL(path)
+        P32, P64 = C.POINTER(C.c_int32), C.POINTER(C.c_int64)
+        lib.korch_select_exact.argtypes = [C.c_int32, C.c_int32, P32, P32, P32, P64, C.c_int32, P32, C.c_int64,
+                                           C.c_double, P64, P32, P64]
+        lib.korch_select_exact.restype = C.c_int32
+        _SEL_LIB = lib
+    return _SEL_LIB
+
+
+def solve_exact(cands, costs, outputs, live=None, time_limit=60.0, max_states=20_000_000):
+    """Exact optimum by the native A* search over producer assignments
+    (libkorch_select.so).  Returns (objective_ns, selection) or None when a limit was
+    reached before optimality was proven."""
+    live = [i for i, c in enumerate(costs) if c < INF] if live is None else list(live)
+    # tensor numbering: a topological order of the "input -> output" relation of the
+    # live candidates (inputs always precede the output in the primitive DAG)
+    tensors = sorted({cands[i]["output"] for i in live} | {j for i in live for j in cands[i]["inputs"]} |
+                     set(outputs))
+    succ = {t: [] for t in tensors}
+    indeg = {t: 0 for t in tensors}
+    edges = set()
+    for i in live:
+        for j in cands[i]["inputs"]:
+            if (j, cands[i]["output"]) not in edges:
+                edges.add((j, cands[i]["output"]))
+                succ[j].append(cands[i]["output"])
+                indeg[cands[i]["output"]] += 1
+    import heapq
+    ready = [t for t in tensors if indeg[t] == 0]
+    heapq.heapify(ready)
+    order = []
+    while ready:
+        t = heapq.heappop(ready)
+        order.append(t)
+        for w in succ[t]:
+            indeg[w] -= 1
+            if indeg[w] == 0:
+                heapq.heappush(ready, w)
+    if len(order) != len(tensors) or len(tensors) > 512:
+        return None
+    loc = {t: k for k, t in enumerate(order)}
+    m = len(live)
+    out = (C.c_int32 * max(1, m))(*[loc[cands[i]["output"]] for i in live])
+    off, ins = [0], []
+    for i in live:
+        ins.extend(loc[j] for j in cands[i]["inputs"])
+        off.append(len(ins))
+    off_a = (C.c_int32 * (m + 1))(*off)
+    in_a = (C.c_int32 * max(1, len(ins)))(*ins)
+    cost_a = (C.c_int64 * max(1, m))(*[int(costs[i]) for i in live])
+    req = sorted({loc[t] for t in outputs})
+    req_a = (C.c_int32 * max(1, len(req)))(*req)
+    best, nexp = C.c_int64(), C.c_int64()
+    sel = (C.c_int32 * max(1, m))()
+    st = _select_lib().korch_select_exact(len(order), m, out, off_a, in_a, cost_a, len(req), req_a, max_states,
+                                          float(time_limit), C.byref(best), sel, C.byref(nexp))
+    global LAST_EXPANDED
+    LAST_EXPANDED += nexp.value
+    if st == -6:
+        raise ValueError("infeasible: some required tensor has no generable producer chain")
+    if st != 0:
+        return None
+    chosen = sorted(live[k] for k in range(m) if sel[k])
+    return int(best.value), chosen
+
+
+LAST_EXPANDED = 0  # A* states expanded by the last solve (all parts)
+LAST_SOLVER = ""   # "exact" (native A*) or "highs" for the last solve
 
 
 def prune_dominated(cands, costs, live):
@@ -56,11 +136,23 @@ def prune_dominated(cands, costs, live):
     return sorted(alive)
 
 
-def solve_blp(cands, costs, outputs, time_limit=600.0):
+def solve_blp(cands, costs, outputs, time_limit=600.0, exact=True, exact_time_limit=120.0):
     """cands: list of dicts with 'output' and 'inputs'; costs: int ns (INF = rejected).
 
+    Exact reductions first (prune_dominated), then the native exact A* search
+    (solve_exact); HiGHS on the MILP only if the search hits its limits.
     Returns (objective_ns, sorted list of selected candidate indices)."""
+    global LAST_OPTIMAL, LAST_GAP, LAST_SOLVER
     live = prune_dominated(cands, costs, [i for i, c in enumerate(costs) if c < INF])
+    for t in outputs:
+        if not any(cands[i]["output"] == t for i in live):
+            raise ValueError(f"infeasible: output p{t} has no generable producer")
+    if exact:
+        r = solve_exact(cands, costs, outputs, live, time_limit=min(time_limit, exact_time_limit))
+        if r is not None:
+            LAST_SOLVER = "exact" if LAST_SOLVER in ("", "exact") else "mixed"
+            return r
+    LAST_SOLVER = "highs" if LAST_SOLVER in ("", "highs") else "mixed"
     idx = {i: k for k, i in enumerate(live)}
     m = len(live)
     producers = {}
@@ -96,7 +188,6 @@ def solve_blp(cands, costs, outputs, time_limit=600.0):
                options={"time_limit": time_limit, "mip_rel_gap": 0.0})
     if res.x is None:
         raise RuntimeError(f"HiGHS failed: {res.message}")
-    global LAST_OPTIMAL, LAST_GAP
     LAST_OPTIMAL = LAST_OPTIMAL and res.status == 0  # 0 = optimal; 1 = time limit (best found)
     gap = getattr(res, "mip_gap", 0.0)
     LAST_GAP = max(LAST_GAP, float(gap) if gap is not None and res.status != 0 else 0.0)
@@ -114,8 +205,8 @@ def solve_partitioned(cands, costs, outputs, time_limit=600.0):
     Parts interact only through cut tensors (a part's primitives consumed by a later
     part), so the global optimum is the sum of per-part optima with
     T_part = (graph outputs in the part) + (its primitives consumed by later parts)."""
-    global LAST_OPTIMAL, LAST_GAP
-    LAST_OPTIMAL, LAST_GAP = True, 0.0
+    global LAST_OPTIMAL, LAST_GAP, LAST_EXPANDED, LAST_SOLVER
+    LAST_OPTIMAL, LAST_GAP, LAST_EXPANDED, LAST_SOLVER = True, 0.0, 0, ""
     parts = sorted({c.get("part", 0) for c in cands})
     if len(parts) <= 1:
         return solve_blp(cands, costs, outputs, time_limit)

@@ -567,6 +567,108 @@ def test_cold_l2_profile_is_finite(ctx):
     assert all(c >= 0.5 * w for c, w in zip(cold, warm))
 
 
+def _ieee_values(shape, rng):
+    """Specials mixed into N(0,1): +-1000 (exp overflows in fp32 AND fp64, so fused
+    fp32 intermediates and the oracle's fp64 ones agree), +-inf, NaN, +-0."""
+    v = rng.standard_normal(shape)
+    specials = np.array([1000.0, -1000.0, np.inf, -np.inf, np.nan, 0.0, -0.0])
+    mask = rng.random(shape) < 0.25
+    v[mask] = specials[rng.integers(0, len(specials), mask.sum())]
+    return v
+
+
+def _assert_ieee_equal(got, want, rtol):
+    """NaN exactly where the oracle has NaN, +-inf where it has +-inf, finite values within
+    rtol of the largest finite oracle magnitude."""
+    np.testing.assert_array_equal(np.isnan(got), np.isnan(want))
+    inf = np.isinf(want)
+    np.testing.assert_array_equal(np.isinf(got), inf)
+    np.testing.assert_array_equal(got[inf], want[inf])
+    fin = np.isfinite(want)
+    if fin.any():
+        scale = max(np.max(np.abs(want[fin])), 1e-30)
+        assert np.max(np.abs(got[fin] - want[fin])) <= rtol * scale
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("dtype", ["f32", "bf16"])
+def test_ieee_special_values_propagate(ctx, dtype):
+    """korch.h promises IEEE propagation: x / 0 = +-inf, 0 / 0 = NaN, exp overflow = inf,
+    the literal softmax (reading A9) turns an overflowing row into inf / inf = NaN, ReLU
+    and sqrt keep NaN, sqrt(-1) = NaN.  Every candidate of the graph inside a feasible
+    orchestration, element by element against the oracle."""
+    from korch_workloads.inputs import bf16_bits_to_f32, bf16_round_bits
+    from paper_2406_09465_b200 import torch_inputs
+    b = GraphBuilder(dtype)
+    x = b.input("x", [16, 64])
+    y = b.input("y", [16, 64])
+    b.output(b.op("Div", x, y))
+    b.output(b.op("Softmax", x, axis=1))
+    b.output(b.op("Relu", b.op("Exp", x)))
+    b.output(b.op("Sqrt", b.op("Relu", x)))
+    b.output(b.op("Sqrt", x))
+    g = b.build()
+    c = Case(ctx, g)
+    rng = np.random.default_rng(11)
+    xv = _ieee_values((16, 64), rng)
+    yv = rng.standard_normal((16, 64))
+    yv[rng.random((16, 64)) < 0.3] = 0.0
+    vals, store = {}, {}
+    for n, v in (("x", xv), ("y", yv)):
+        v32 = v.astype(np.float32)
+        if dtype == "bf16":
+            bits = bf16_round_bits(v32)
+            vals[n], store[n] = bf16_bits_to_f32(bits).astype(np.float64), bits
+        else:
+            vals[n], store[n] = v32.astype(np.float64), v32
+    c.values = vals
+    c.dev_in = torch_inputs(g, store)
+    gen = [x_["index"] for x_ in c.cands if x_["klass"] != "rejected"]
+    sels = {tuple(c.kg.singletons()), tuple(c.kg.operator_aligned())}
+    sels |= {tuple(c.completion([i])) for i in gen}
+    with np.errstate(all="ignore"):
+        for sel in sorted(sels):
+            got = c.run(list(sel))
+            want = c.oracle(list(sel))
+            for k, o in enumerate(c.kg.outputs):
+                _assert_ieee_equal(got[k], want[o], RTOL[dtype])
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("which", ["c1", "c2_small_pairs"])
+def test_selection_on_measured_costs_equals_oracle_search(ctx, which):
+    """P:377-413 on MEASURED costs: after on-device profiling, the product's selection
+    (native exact search) and the HiGHS MILP both reach exactly the objective of the
+    oracle's independent producer-assignment search on the same integer-ns cost vector,
+    and the selection is feasible (Eq. 3/4) and accepted by the library."""
+    from oracle.enumeration import candidate_inputs
+    from oracle.orchestration import feasible, producer_search
+    from paper_2406_09465_b200 import INF, solve_blp
+    if which == "c1":
+        g, kw = c1_softmax_layernorm(), {}
+    else:
+        g, kw = c2_vit_attention(seq=32, hidden=128, heads=2), {"attention_pairs": True}
+    from paper_2406_09465_b200 import KorchGraph
+    kg = KorchGraph(ctx, g)
+    cands = kg.enumerate(**kw)
+    costs = kg.profile()
+    pg = fission(g)
+    G = PGraph(pg)
+    ref = candidates(G, convex_sets_from_states(execution_states(G)), attention_pairs=bool(kw))
+    assert [(tuple(c["members"]), c["output"]) for c in cands] == [(tuple(m), o) for m, o in ref]
+    gen = [i for i, c in enumerate(costs) if c < INF]
+    sub = [ref[i] for i in gen]
+    cin = [candidate_inputs(G, m) for m, _ in sub]
+    best, _ = producer_search(sub, [costs[i] for i in gen], pg["outputs"], cin, G.topo_index)
+    obj, sel = kg.select(costs)
+    assert obj == best
+    cin_all = [candidate_inputs(G, m) for m, _ in ref]
+    assert feasible(ref, sel, pg["outputs"], cin_all)
+    hi, hsel = solve_blp(cands, costs, kg.outputs, exact=False)
+    assert hi == best and feasible(ref, hsel, pg["outputs"], cin_all)
+    kg.set_orchestration(sel)
+
+
 @pytest.mark.gpu
 def test_execute_host_matches_execute(ctx):
     """korch_execute_host (H2D of the activation, the plan, D2H of the output in one graph
@@ -595,6 +697,41 @@ def test_execute_host_matches_execute(ctx):
         c.kg.execute(ref_in, ref, ws, torch.cuda.current_stream())
         torch.cuda.synchronize()
         assert torch.equal(host_out[0], ref[0].cpu())
+
+
+@pytest.mark.gpu
+def test_execute_host_back_to_back_distinct_inputs(ctx):
+    """korch_execute_host called back to back with a different activation per call and no
+    synchronisation in between: the plan's residual GEMM fetches x before its dependency
+    wait, so it must not overlap the H2D copy of x.  Every call's output must
+    equal korch_execute on that call's input."""
+    import torch
+    c = Case(ctx, c2_vit_attention())
+    costs = c.kg.profile()
+    _, sel = c.kg.select(costs)
+    c.kg.set_orchestration(sel)
+    ws = c.kg.torch_workspace()
+    names = [s["name"] for s in c.graph["inputs"]]
+    xi = names.index("x")
+    gen = torch.Generator().manual_seed(7)
+    xs = [torch.randn(c.dev_in[xi].shape, generator=gen).to(c.dev_in[xi].dtype).pin_memory() for _ in range(6)]
+    dev = list(c.dev_in)
+    dev[xi] = torch.empty_like(c.dev_in[xi])
+    outs = c.kg.torch_outputs()
+    host_out = torch.empty((len(xs),) + tuple(outs[0].shape), dtype=outs[0].dtype).pin_memory()
+    stream = torch.cuda.current_stream()
+    for rep in range(2):  # the second round replays the captured graphs
+        for k, xh in enumerate(xs):
+            hin = [xh if i == xi else None for i in range(len(names))]
+            c.kg.execute_host(hin, dev, [host_out[k]], outs, ws, stream)
+        torch.cuda.synchronize()
+        for k, xh in enumerate(xs):
+            ref_in = list(c.dev_in)
+            ref_in[xi] = xh.cuda()
+            ref = c.kg.torch_outputs()
+            c.kg.execute(ref_in, ref, ws, stream)
+            torch.cuda.synchronize()
+            assert torch.equal(host_out[k], ref[0].cpu()), (rep, k)
 
 
 def _gemm_graph(m, k, n, batch=1, act="Relu"):

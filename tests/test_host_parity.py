@@ -186,6 +186,61 @@ def test_blp_pruning_exact_on_random_graphs(ctx):
         assert feasible(ref, sel, G.pg["outputs"], cin)
 
 
+def test_exact_solver_equals_highs_and_oracle(ctx):
+    """The native A* search (libkorch_select.so) and the HiGHS MILP reach the same
+    objective as the oracle's producer-assignment search on random DAGs and C1, with
+    costs that tie often (3 values) and costs that rarely tie; the A* selection also has
+    the fewest kernels among equal-cost optima (reading A8: the oracle's tie-break)."""
+    from paper_2406_09465_b200.select import prune_dominated, solve_exact
+    rng = np.random.default_rng(17)
+    graphs = [_random_op_graph(rng, int(rng.integers(2, 7))) for _ in range(15)] + [c1_softmax_layernorm()]
+    for gi, g in enumerate(graphs):
+        kg = KorchGraph(ctx, g)
+        mp = 16 if gi == len(graphs) - 1 else 8   # C1 at the default max_prims
+        cands = kg.enumerate(max_prims=mp)
+        G, ref = _oracle_cands(g, max_prims=mp)
+        cin = [candidate_inputs(G, m) for m, _ in ref]
+        for tie in (True, False):
+            costs = [int(rng.integers(1, 4)) * 1000 if tie else int(rng.integers(1000, 9000)) for _ in cands]
+            best, osel = producer_search(ref, costs, G.pg["outputs"], cin, G.topo_index)
+            ex = solve_exact(cands, costs, kg.outputs)
+            assert ex is not None
+            assert ex[0] == best and feasible(ref, ex[1], G.pg["outputs"], cin)
+            assert len(ex[1]) == len(osel)
+            live = prune_dominated(cands, costs, range(len(cands)))
+            ex2 = solve_exact(cands, costs, kg.outputs, live)
+            assert ex2[0] == best and len(ex2[1]) == len(osel)
+            hi, hsel = solve_blp(cands, costs, kg.outputs, exact=False)
+            assert hi == best and feasible(ref, hsel, G.pg["outputs"], cin)
+
+
+def test_exact_solver_whole_model_equals_highs(ctx):
+    """Candy at its paper size (224^2, 2886 partitioned candidates): the exact A* search
+    and HiGHS (proven optimal within its limit) agree on every part with analytic
+    synthetic costs (bytes / 6.5 GB/ms + flops / 1.5 TFLOP/ms + 2 us + noise)."""
+    import paper_2406_09465_b200.select as S
+    from korch_workloads.models import candy
+    kg = KorchGraph(ctx, candy())
+    frag = {}
+    for n in kg.prim["nodes"]:
+        frag[n["op"]] = frag.get(n["op"], 0) + 1
+    cands = kg.enumerate(partition_max=64, max_prims=max(12, max(frag.values())))
+    rng = np.random.default_rng(0)
+    costs = [S.INF if c["klass"] == "rejected" else
+             int(2000 + c["bytes"] / 6.5 + c["flops"] / 1.5e6 + rng.integers(0, 800)) for c in cands]
+    obj, sel = S.solve_partitioned(cands, costs, kg.outputs)
+    assert S.LAST_SOLVER == "exact" and S.LAST_OPTIMAL
+    kg.set_orchestration(sel)
+    orig = S.solve_blp
+    try:
+        S.solve_blp = lambda c, co, o, tl=600.0: orig(c, co, o, tl, exact=False)
+        obj2, sel2 = S.solve_partitioned(cands, costs, kg.outputs, time_limit=300)
+        assert S.LAST_SOLVER == "highs" and S.LAST_OPTIMAL
+    finally:
+        S.solve_blp = orig
+    assert obj == obj2 and len(sel) <= len(sel2)
+
+
 @pytest.mark.parametrize("name,pm", [("c2", 8), ("c2", 12), ("c2_r1r3", 10), ("misc", 6), ("c1", 5)])
 def test_partitioned_enumeration_matches_oracle(ctx, name, pm):
     from oracle.enumeration import candidates_partitioned, partition
