@@ -183,86 +183,193 @@ def time_plan(kg, sel, dev_in, steps=20, flush_mb=512):
 
 
 MODEL_MAX_PRIMS = 12  # SPEC S:393's default; whole models only (reading A5)
+DEFAULT_MODELS = ["candy", "efficientvit", "yolox", "segformer", "efficientvit2048"]
+TUNING_DB = os.path.join(ROOT, "profiles", "tuning_db")
 
 
-def run_models(K, names, oracle_check=True, blp_time_limit=30.0):
-    """Whole paper models at their paper input sizes, bs = 1: partition,
-    enumerate, compile, profile, BLP-select, then measure the chosen orchestration and the
-    operator-aligned one (one kernel per unfused operator) end to end."""
+def model_graph(name: str, batch: int = 1):
+    from korch_workloads.models import MODELS
+    if batch != 1:
+        raise ValueError("whole models are built at batch 1")
+    return MODELS[name]()
+
+
+def model_enum_opts(kg) -> dict:
+    """Enumeration options for whole models: partitioned (reading A17, <= 64 primitives
+    per part) and max_prims = 12, raised to the largest operator fragment so
+    the one-kernel-per-operator baseline stays in the candidate set (reading A5)."""
+    frag = {}
+    for n in kg.prim["nodes"]:
+        frag[n["op"]] = frag.get(n["op"], 0) + 1
+    return {"partition_max": 64, "max_prims": max(MODEL_MAX_PRIMS, max(frag.values()))}
+
+
+def timed_steps(fn, stream, steps, flush):
+    """Per-step device ms (CUDA events on `stream`), L2 flushed between steps outside the
+    events."""
+    import torch
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(steps)]
+    torch.cuda.synchronize()
+    for i, (a, e) in enumerate(ev):
+        flush.fill_(i & 0xFF)
+        a.record(stream)
+        fn()
+        e.record(stream)
+    torch.cuda.synchronize()
+    return [a.elapsed_time(e) for a, e in ev]
+
+
+def dist_summary(ts):
+    qs = sorted(ts)
+
+    def pct(q):
+        return qs[min(len(qs) - 1, int(round(q * (len(qs) - 1))))]
+    return {"mean": statistics.mean(ts), "p10": pct(0.1), "p50": statistics.median(ts), "p90": pct(0.9)}
+
+
+def roofline_of(kg, cands, i, cold_ns, pk):
+    """Roofline of candidate i from its algorithmic bytes / flops and a cold-L2 time."""
+    c = cands[i]
+    ridge = pk["bf16_tflops"] * 1e12 / (pk["hbm_gbs"] * 1e9)
+    ai = c["flops"] / max(1, c["bytes"]) if c["klass"] == "gemm" else 0.0
+    if ai > ridge:
+        ach = c["flops"] / (cold_ns * 1e-9) / 1e12
+        r = {"bound": "tensor", "achieved": ach, "peak": pk["bf16_tflops"], "unit": "TFLOP/s"}
+    else:
+        ach = c["bytes"] / (cold_ns * 1e-9) / 1e9
+        r = {"bound": "hbm", "achieved": ach, "peak": pk["hbm_gbs"], "unit": "GB/s"}
+    r["frac"] = r["achieved"] / r["peak"]
+    name = kg.kernel_name(i)
+    r.update({"traffic": load_ncu_traffic(name), "candidate": i, "class": c["klass"], "members": len(c["members"]),
+              "algorithmic_bytes": c["bytes"], "flops": c["flops"], "ns_cold_l2": cold_ns, "name": name,
+              "variant": kg.variant_info(i)[2]})
+    return r
+
+
+def run_model(K, name, pk, steps=50, oracle_check=True, retune=False, db_dir=TUNING_DB, flush=None):
+    """One paper model at its paper input size, bs 1: partitioned enumeration,
+    costs from the tuning database (tunedb.py; recorded on a B200 by tools/tune_models.py,
+    P:629) or profiled live, exact Eq. 2-4 selection, then the chosen orchestration and the
+    operator-aligned one (one kernel per unfused operator) timed end to end with L2 flushed
+    between steps and clocks sampled; output checked against the fp64 oracle."""
     import numpy as np
     import torch
+    import paper_2406_09465_b200.select as S
     from korch_workloads import make_inputs
-    from korch_workloads.models import MODELS
-    os.environ["KORCH_CACHE_DIR"] = os.environ.get(
-        "KORCH_MODEL_CACHE", os.path.join(ROOT, "paper_2406_09465_b200", "kcache_models"))
-    os.makedirs(os.environ["KORCH_CACHE_DIR"], exist_ok=True)
-    res = {}
-    for name in names:
-        t0 = time.perf_counter()
-        graph = MODELS[name]()
-        ctx = K.Context(torch.cuda.current_device())
-        kg = K.KorchGraph(ctx, graph)
-        # the operator-aligned baseline needs every operator's fragment as a candidate
-        frag = {}
-        for n in kg.prim["nodes"]:
-            frag[n["op"]] = frag.get(n["op"], 0) + 1
-        cands = kg.enumerate(partition_max=64, max_prims=max(MODEL_MAX_PRIMS, max(frag.values())))
-        t_enum = time.perf_counter() - t0
-        t1 = time.perf_counter()
+    from paper_2406_09465_b200 import tunedb
+    t0 = time.perf_counter()
+    graph = model_graph(name)
+    ctx = K.Context(torch.cuda.current_device())
+    kg = K.KorchGraph(ctx, graph)
+    opts = model_enum_opts(kg)
+    cands = kg.enumerate(**opts)
+    t_enum = time.perf_counter() - t0
+    db_path = os.path.join(db_dir, f"{name}_b1.json")
+    db = None if retune else tunedb.load(db_path)
+    ok, why = tunedb.usable(db, graph, opts)
+    t1 = time.perf_counter()
+    if ok:
+        costs, missing = tunedb.apply(kg, db)
+        if missing:
+            live = kg.profile(missing)
+            for i, c in zip(missing, live):
+                costs[i] = c
+        tuning = {"source": f"tuning database {os.path.relpath(db_path, ROOT)} (recorded {db.get('created')} on "
+                            f"{db.get('device')}, {len(db['kernels'])} kernels)", "profiled_live": len(missing),
+                  "recorded_tuning_s": db.get("tuning_s")}
+    else:
         kg.compile()
-        t_comp = time.perf_counter() - t1
-        t1 = time.perf_counter()
         costs = kg.profile()
-        t_prof = time.perf_counter() - t1
-        print(f"[models] {name}: {len(cands)} candidates, enumerate {t_enum:.0f}s, compile {t_comp:.0f}s, "
-              f"profile {t_prof:.0f}s", file=sys.stderr, flush=True)
-        t1 = time.perf_counter()
-        obj, sel = kg.select(costs, time_limit=blp_time_limit)
-        t_sel = time.perf_counter() - t1
-        import paper_2406_09465_b200.select as S
-        blp_optimal, blp_gap = S.LAST_OPTIMAL, S.LAST_GAP
-        base = kg.operator_aligned()
-        ins = make_inputs(graph, seed=0)
-        dev = K.torch_inputs(graph, {k: v[1] for k, v in ins.items()})
-        ms_sel, outs = time_plan(kg, sel, dev)
-        got = [o.float().cpu().numpy().astype(np.float64) for o in outs]
-        ms_base, _ = time_plan(kg, base, dev)
-        entry = {"input": graph["inputs"][0]["shape"], "n_prims": kg.n_prims, "n_candidates": len(cands),
-                 "n_generable": len(kg.generable()), "n_states": kg.n_states,
-                 "parts": len({c["part"] for c in cands}),
-                 "latency_ms": ms_sel, "kernels": len(sel),
-                 "operator_aligned_ms": ms_base, "operator_aligned_kernels": len(base),
-                 "speedup_vs_operator_aligned": ms_base / ms_sel,
-                 "blp_objective_ns": obj, "blp_optimal": blp_optimal, "blp_max_rel_gap": blp_gap,
-                 "blp_time_limit_s_per_part": blp_time_limit,
-                 "operator_aligned_objective_ns": sum(costs[i] for i in base),
-                 "compile_failures": len(kg.compile_failures),
-                 "tuning_s": {"enumerate": t_enum, "compile": t_comp, "profile": t_prof, "select": t_sel}}
-        kinds = {n["id"]: n["kind"] for n in kg.prim["nodes"]}
+        tuning = {"source": f"profiled live ({why})", "profiled_live": len(cands)}
+    tuning["profile_s"] = time.perf_counter() - t1
+    t1 = time.perf_counter()
+    obj, sel = kg.select(costs)
+    tuning.update({"enumerate_s": t_enum, "select_s": time.perf_counter() - t1, "solver": S.LAST_SOLVER,
+                   "search_states": S.LAST_EXPANDED})
+    blp_optimal, blp_gap = S.LAST_OPTIMAL, S.LAST_GAP
+    base = kg.operator_aligned()
+    ins = make_inputs(graph, seed=0)
+    dev = K.torch_inputs(graph, {k: v[1] for k, v in ins.items()})
+    stream = torch.cuda.current_stream()
+    if flush is None:
+        flush = torch.empty(512 << 20, dtype=torch.uint8, device="cuda")
+    res = {"input": graph["inputs"][0]["shape"], "n_prims": kg.n_prims, "n_candidates": len(cands),
+           "n_generable": len(kg.generable()), "n_states": kg.n_states, "parts": len({c["part"] for c in cands})}
 
-        def top(plan, n=6):
-            return [{"cand": i, "ns": costs[i], "class": cands[i]["klass"], "bytes": cands[i]["bytes"],
-                     "flops": cands[i]["flops"], "kinds": [kinds[m] for m in cands[i]["members"]],
-                     "variant": kg.variant_info(i)[2]} for i in sorted(plan, key=lambda i: -costs[i])[:n]]
-        entry["slowest_selected"] = top(sel)
-        entry["slowest_operator_aligned"] = top(base)
-        if oracle_check:
-            from oracle.enumeration import PGraph
-            from oracle.evaluate import eval_orchestration
-            from oracle.fission import fission
-            t1 = time.perf_counter()
-            pg = fission(graph)
-            G = PGraph(pg)
-            want = eval_orchestration(pg, [(tuple(c["members"]), c["output"]) for c in cands], sel,
-                                      {k: v[0] for k, v in ins.items()}, G.topo_index, graph["dtype"])
-            errs = [float(np.max(np.abs(g - want[o])) / np.max(np.abs(want[o]))) for g, o in zip(got, kg.outputs)]
-            entry["oracle_rel_err"] = max(errs)
-            entry["oracle_s"] = time.perf_counter() - t1
-        res[name] = entry
-        print("[models] " + json.dumps({name: entry}), file=sys.stderr, flush=True)
-        del kg, outs, dev
-        ctx.close()
-        torch.cuda.empty_cache()
+    def measure(plan):
+        kg.set_orchestration(plan)
+        outs, ws = kg.torch_outputs(), kg.torch_workspace()
+        for _ in range(5):
+            kg.execute(dev, outs, ws, stream)
+        with Clocks(torch.cuda.current_device()) as clk:
+            ts = timed_steps(lambda: kg.execute(dev, outs, ws, stream), stream, steps, flush)
+            # keep the GPU busy until the sampler has seen the load
+            t_end = time.perf_counter()
+            while time.perf_counter() - t_end < 0.25:
+                for _ in range(20):
+                    kg.execute(dev, outs, ws, stream)
+                torch.cuda.synchronize()
+        return dist_summary(ts), clk.summary(), outs, ws
+    lat, clocks, outs, ws = measure(sel)
+    got = [o.float().cpu().numpy().astype(np.float64) for o in outs]
+    order = kg.plan()
+    # e2e through korch_execute_host: the image H2D from pinned memory, the plan, and the
+    # output written straight into pinned host memory, every step
+    xi = [s["name"] for s in graph["inputs"]].index("x")
+    host_x = dev[xi].cpu().pin_memory()
+    host_out = [torch.empty_like(o, device="cpu").pin_memory() for o in outs]
+    hin = [host_x if i == xi else None for i in range(len(dev))]
+    dev_e2e = list(dev)
+    dev_e2e[xi] = torch.empty_like(dev[xi])
+    for _ in range(3):
+        kg.execute_host(hin, dev_e2e, host_out, outs, ws, stream)
+    e2e = timed_steps(lambda: kg.execute_host(hin, dev_e2e, host_out, outs, ws, stream), stream, max(10, steps // 2),
+                      flush)
+    torch.cuda.synchronize()
+    e2e_match = all(torch.equal(h, g.cpu()) or torch.equal(h.float(), torch.from_numpy(r).to(h.dtype).float())
+                    for h, g, r in zip(host_out, outs, got))
+    # plan roofline T*(u) = sum_i max(B_i / BW, F_i / P) (SURVEY.md §8(d))
+    t_star = sum(max(cands[i]["bytes"] / pk["hbm_gbs"], cands[i]["flops"] / (pk["bf16_tflops"] * 1e3)) for i in order)
+    dom = max(order, key=lambda i: costs[i])
+    dom_cold = kg.profile([dom], flush_l2=True, trials=7, tune=False)[0]
+    kinds = {n["id"]: n["kind"] for n in kg.prim["nodes"]}
+    top = [{"cand": i, "ns": costs[i], "class": cands[i]["klass"], "bytes": cands[i]["bytes"],
+            "flops": cands[i]["flops"], "kinds": [kinds[m] for m in cands[i]["members"]],
+            "variant": kg.variant_info(i)[2], "name": kg.kernel_name(i)}
+           for i in sorted(order, key=lambda i: -costs[i])[:5]]
+    base_lat, base_clocks, _, _ = measure(base)
+    res.update({"latency_ms": lat["p50"], "latency_ms_dist": lat, "clocks": clocks, "kernels": len(order),
+                "e2e_ms": statistics.median(e2e), "e2e_h2d_bytes": host_x.numel() * host_x.element_size(),
+                "e2e_d2h_bytes": sum(t.numel() * t.element_size() for t in host_out), "e2e_output_matches": e2e_match,
+                "operator_aligned_ms": base_lat["p50"], "operator_aligned_ms_dist": base_lat,
+                "operator_aligned_kernels": len(base), "operator_aligned_clocks": base_clocks,
+                "speedup_vs_operator_aligned": base_lat["p50"] / lat["p50"],
+                "blp_objective_ns": obj, "operator_aligned_objective_ns": sum(costs[i] for i in base),
+                "blp_optimal": blp_optimal, "blp_max_rel_gap": blp_gap,
+                "plan_roofline": {"t_star_us": t_star / 1e3, "frac_of_t_star": t_star / (lat["p50"] * 1e6),
+                                  "bytes": sum(cands[i]["bytes"] for i in order),
+                                  "flops": sum(cands[i]["flops"] for i in order)},
+                "dominant": roofline_of(kg, cands, dom, dom_cold, pk), "slowest_selected": top,
+                "tuning": tuning})
+    if oracle_check:
+        from oracle.enumeration import PGraph
+        from oracle.evaluate import eval_orchestration
+        from oracle.fission import fission
+        t1 = time.perf_counter()
+        pg = fission(graph)
+        G = PGraph(pg)
+        want = eval_orchestration(pg, [(tuple(c["members"]), c["output"]) for c in cands], sel,
+                                  {k: v[0] for k, v in ins.items()}, G.topo_index, graph["dtype"])
+        errs = [float(np.max(np.abs(g - want[o])) / np.max(np.abs(want[o]))) for g, o in zip(got, kg.outputs)]
+        res["oracle_rel_err"] = max(errs)
+        res["oracle_tol"] = 2e-2 if graph["dtype"] == "bf16" else 1e-4
+        res["oracle_s"] = time.perf_counter() - t1
+    res["wall_s"] = time.perf_counter() - t0
+    print("[models] " + json.dumps({name: {k: res[k] for k in ("latency_ms", "operator_aligned_ms", "kernels",
+                                                             "blp_optimal", "wall_s")}}), file=sys.stderr, flush=True)
+    del kg, outs, dev, ws
+    ctx.close()
+    torch.cuda.empty_cache()
     return res
 
 
@@ -416,6 +523,19 @@ def run_reference(args):
     return 0
 
 
+def spawn_ranks(n: int) -> int:
+    """`bench.py --gpus N` started without a launcher: start N ranks (one process per GPU)
+    the way the driver does, `torch.distributed.run` on 127.0.0.1, with the same
+    arguments; rank 0 prints the JSON line."""
+    import socket
+    with socket.socket() as sk:
+        sk.bind(("127.0.0.1", 0))
+        port = sk.getsockname()[1]
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={n}",
+           "--master-addr=127.0.0.1", f"--master-port={port}", os.path.abspath(__file__)] + sys.argv[1:]
+    return subprocess.call(cmd)
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -425,7 +545,9 @@ def main():
     ap.add_argument("--impl", default="korch", choices=["korch", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-bw-variant", action="store_true", help="skip the C1 x[2^20,128] bandwidth measurement")
-    ap.add_argument("--models", default="", help="comma list of whole models to tune and time (candy,segformer)")
+    ap.add_argument("--models", default=",".join(DEFAULT_MODELS),
+                    help="comma list of whole paper models to time at bs 1 ('' = none)")
+    ap.add_argument("--retune", action="store_true", help="profile the models live instead of using the tuning database")
     ap.add_argument("--no-scaled", action="store_true", help="skip the C2 batch-64 measurement")
     ap.add_argument("--no-attention-pairs", action="store_true",
                     help="paper-faithful P:626 prune only (no fused two-GEMM attention candidates)")
@@ -433,6 +555,8 @@ def main():
     ap.add_argument("--save-selection", default=None, help="write the chosen plan (for tools/replay.py)")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        return spawn_ranks(args.gpus)
     if args.impl == "reference":
         return run_reference(args)
 
@@ -641,8 +765,22 @@ def main():
         base_ms, _ = time_plan(kg, base, dev_in, steps=args.steps)
         kg.set_orchestration(sel)
     models = None
-    if rank == 0 and world == 1 and args.models:
-        models = run_models(K, [m for m in args.models.split(",") if m])
+    if args.models:
+        # every rank runs every model (bs 1 does not shard: replicas); the reported latency
+        # is the max over ranks of each rank's median step (G4)
+        models = {}
+        for m in [m for m in args.models.split(",") if m]:
+            try:
+                models[m] = run_model(K, m, pk, steps=max(20, args.steps), retune=args.retune, flush=flush,
+                                      oracle_check=rank == 0)
+                lat = models[m]["latency_ms"]
+            except Exception as e:  # reported, never silently replaced
+                models[m] = {"error": f"{type(e).__name__}: {e}"[:400]}
+                lat = float("nan")
+            if world > 1:
+                lat_max, = max_over_ranks([lat], device=coll_dev)
+                models[m]["latency_ms_rank0"] = models[m].get("latency_ms")
+                models[m]["latency_ms"] = lat_max
     scaled = None
     if not args.no_scaled and args.config == "c2":
         try:

@@ -173,6 +173,14 @@ korch_status korch_variant_info(const korch_graph* g, int64_t i, int32_t* n_vari
  * was not profiled, INT64_MAX if it failed to launch). */
 korch_status korch_variant_cost(const korch_graph* g, int64_t i, int32_t v, int64_t* ns);
 
+/* Kernel (entry-point) name of launch variant v of candidate i: a hash of the kernel's
+ * generated source, i.e. of everything that determines what it computes and how it is
+ * launched (with the shared prelude fixed; see korch_version).  Used as the key of
+ * profiled costs in a tuning database.  Same buffer protocol as
+ * korch_graph_dump; KORCH_E_ARG if i or v is out of range. */
+korch_status korch_variant_name(const korch_graph* g, int64_t i, int32_t v, char* name, size_t cap,
+                                size_t* needed);
+
 /* Force candidate i to use launch variant v (e.g. to replay a plan without
  * re-profiling).  Takes effect at the next korch_set_orchestration. */
 korch_status korch_select_variant(korch_graph* g, int64_t i, int32_t v);

@@ -8,6 +8,7 @@ point fails loudly (ImportError) when libkorch.so is missing.
 """
 _API = ("Context", "KorchGraph", "torch_inputs")
 _SELECT = ("INF", "operator_aligned", "singletons", "solve_blp")
+_MODULES = ("tunedb", "select", "dist")
 __all__ = list(_API + _SELECT)
 
 
@@ -15,6 +16,9 @@ def __getattr__(name):
     if name in _API:
         from . import api
         return getattr(api, name)
+    if name in _MODULES:
+        import importlib
+        return importlib.import_module(f"{__name__}.{name}")
     if name in _SELECT:
         from . import select
         return getattr(select, name)

@@ -32,7 +32,7 @@ EXPORTS = [
     "korch_graph_free", "korch_graph_info", "korch_graph_dump", "korch_validate", "korch_enumerate",
     "korch_candidate", "korch_candidate_source", "korch_compile", "korch_profile",
     "korch_set_orchestration", "korch_plan", "korch_execute", "korch_variant_info", "korch_select_variant",
-    "korch_variant_cost", "korch_execute_host",
+    "korch_variant_cost", "korch_execute_host", "korch_variant_name",
 ]
 
 
@@ -87,6 +87,7 @@ def load():
         "korch_variant_info": ([P, I64, C.POINTER(I32), C.POINTER(I32), C.c_char_p, SZ], I32),
         "korch_select_variant": ([P, I64, I32], I32),
         "korch_variant_cost": ([P, I64, I32, C.POINTER(I64)], I32),
+        "korch_variant_name": ([P, I64, I32, C.c_char_p, C.c_size_t, C.POINTER(C.c_size_t)], I32),
     }
     for name, (args, res) in sig.items():
         f = getattr(lib, name)

@@ -187,6 +187,17 @@ class KorchGraph:
             out.append(ns.value)
         return out
 
+    def variant_names(self, i: int):
+        """Kernel names of every launch variant of candidate i (tuning-database keys)."""
+        nv, _, _ = self.variant_info(i)
+        buf = C.create_string_buffer(128)
+        need = C.c_size_t()
+        out = []
+        for v in range(nv):
+            check(LIB.korch_variant_name(self.h, i, v, buf, len(buf), C.byref(need)))
+            out.append(buf.value.decode())
+        return out
+
     def set_variant(self, i: int, v: int):
         check(LIB.korch_select_variant(self.h, i, v))
 

@@ -179,7 +179,7 @@ static const char* const kNvrtcOpts[] = {"-arch=sm_100a", "-std=c++17", "-defaul
 // Everything else that goes into the cubin -- the shared prelude, the template, the NVRTC
 // options and the NVRTC version -- salts the cache key, so a change to any of them misses
 // the on-disk cache instead of loading a stale cubin.
-static std::string cache_key(const KernelVariant& v) {
+static const std::array<std::string, 2>& codegen_salt() {
   static const std::array<std::string, 2> salt = [] {
     std::string opts;
     for (const char* o : kNvrtcOpts) opts += std::string(o) + " ";
@@ -192,8 +192,10 @@ static std::string cache_key(const KernelVariant& v) {
                   (unsigned long long)fnv1a(kernel_prelude() + std::string(kSm100GemmTemplate) + opts));
     return std::array<std::string, 2>{a, b};
   }();
-  return v.name + "." + salt[v.tcgen05 ? 1 : 0];
+  return salt;
 }
+
+static std::string cache_key(const KernelVariant& v) { return v.name + "." + codegen_salt()[v.tcgen05 ? 1 : 0]; }
 
 // Batched NVRTC compilation: up to kBatch kernels per program, so the per-program
 // overhead (front-end start-up, prelude and template parsing) is paid once per batch.
@@ -492,7 +494,12 @@ static int64_t tensor_bytes(const Graph& g, const Ref& r) { return numel(g.shape
 // ------------------------------------------------------------------ API
 extern "C" {
 
-const char* korch_version(void) { return "korch-b200 0.1 (sm_100a)"; }
+// the codegen salt identifies the prelude / template / NVRTC options the kernels are built
+// with: profiled costs recorded under another version describe other kernels
+const char* korch_version(void) {
+  static const std::string v = "korch-b200 0.2 (sm_100a) codegen " + codegen_salt()[0] + "-" + codegen_salt()[1];
+  return v.c_str();
+}
 const char* korch_last_error(void) { return g_err.c_str(); }
 
 // KORCH_SEGV_TRACE=1: print a native backtrace on SIGSEGV (diagnostics on the GPU box,
@@ -876,6 +883,14 @@ korch_status korch_variant_cost(const korch_graph* G, int64_t i, int32_t v, int6
   if (v < 0 || v >= (int32_t)s.plan.variants.size()) return fail(KORCH_E_ARG, "variant index out of range");
   *ns = v < (int32_t)s.var_ns.size() ? s.var_ns[v] : -1;
   return KORCH_OK;
+}
+
+korch_status korch_variant_name(const korch_graph* G, int64_t i, int32_t v, char* name, size_t cap, size_t* needed) {
+  if (!G) return fail(KORCH_E_ARG, "NULL graph");
+  if (i < 0 || i >= (int64_t)G->cands.size()) return fail(KORCH_E_ARG, "candidate index out of range");
+  const CandState& s = G->cs[i];
+  if (v < 0 || v >= (int32_t)s.plan.variants.size()) return fail(KORCH_E_ARG, "variant index out of range");
+  return write_buf(s.plan.variants[v].name, name, cap, needed);
 }
 
 korch_status korch_select_variant(korch_graph* G, int64_t i, int32_t v) {

@@ -199,6 +199,44 @@ static __device__ __forceinline__ uint4 ld_bf16x8_unaligned(const unsigned short
   return r;
 }
 
+// shared-memory reads for operands built from a staged tile (the conv halo)
+static __device__ __forceinline__ uint4 ld_shared_v4(unsigned addr) {
+  uint4 v;
+  asm volatile("ld.shared.v4.u32 {%0, %1, %2, %3}, [%4];" : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w) : "r"(addr));
+  return v;
+}
+static __device__ __forceinline__ unsigned short ld_shared_u16(unsigned addr) {
+  unsigned short v;
+  asm volatile("ld.shared.u16 %0, [%1];" : "=h"(v) : "r"(addr));
+  return v;
+}
+// 8 consecutive bf16 at a 2-byte-aligned shared address (two aligned 16-byte reads and
+// a funnel shift; the buffer keeps 16 readable bytes past its last element)
+static __device__ __forceinline__ uint4 ld_shared_bf16x8_unaligned(unsigned addr) {
+  const unsigned off = addr & 15u;
+  const uint4 lo = ld_shared_v4(addr & ~15u);
+  if (off == 0) return lo;
+  const uint4 hi = ld_shared_v4((addr & ~15u) + 16u);
+  const unsigned sh = (off & 3u) * 8u;
+  unsigned w0, w1, w2, w3, w4;
+  switch (off >> 2) {
+    case 0: w0 = lo.x; w1 = lo.y; w2 = lo.z; w3 = lo.w; w4 = hi.x; break;
+    case 1: w0 = lo.y; w1 = lo.z; w2 = lo.w; w3 = hi.x; w4 = hi.y; break;
+    case 2: w0 = lo.z; w1 = lo.w; w2 = hi.x; w3 = hi.y; w4 = hi.z; break;
+    default: w0 = lo.w; w1 = hi.x; w2 = hi.y; w3 = hi.z; w4 = hi.w; break;
+  }
+  uint4 r;
+  r.x = __funnelshift_r(w0, w1, sh);
+  r.y = __funnelshift_r(w1, w2, sh);
+  r.z = __funnelshift_r(w2, w3, sh);
+  r.w = __funnelshift_r(w3, w4, sh);
+  return r;
+}
+// barrier over a subset of warps (id 1..15, n = thread count, a multiple of 32)
+static __device__ __forceinline__ void named_bar_sync(unsigned id, unsigned n) {
+  asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory");
+}
+
 // ---------------------------------------------------------------- clusters / DSMEM
 // full cluster barrier (all threads of every CTA; release/acquire orders DSMEM traffic)
 static __device__ __forceinline__ void cluster_sync() {
