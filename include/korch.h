@@ -67,6 +67,12 @@ typedef struct {
                                  many primitives; 0: only graphs > 256 primitives, parts of 64 */
   int32_t attention_pairs;    /* 1: keep candidates with two MatMuls where the first feeds the
                                  second's A operand (fused attention; NEXT item N2) */
+  int32_t max_outputs;        /* N1 ("for O in P'"; reading A32):
+                                 <= 1: single-output candidates only (default); k > 1 (capped
+                                 at 4): every single-output candidate (P', o) also yields
+                                 (P', o, E) for each non-empty E of at most k - 1 members of
+                                 P' other than o that have a consumer outside P' (or are graph
+                                 outputs) and o's shape; E is materialised too            */
 } korch_enum_opts;
 
 /* One candidate kernel (P', o): a convex set with a unique sink o (reading A4). */
@@ -84,6 +90,8 @@ typedef struct {
   double flops;               /* 2*M*N*K summed over dense linear members                   */
   const char* signature;      /* canonical text of the generated kernel (dedup key)         */
   int32_t part;               /* partition part the candidate lies in (0 if unpartitioned)  */
+  int32_t n_extra_outputs;    /* |E|: secondary materialised outputs (N1, reading A32)      */
+  const int32_t* extra_outputs;/* primitive ids, ascending; the kernel writes them after o    */
 } korch_cand_desc;
 
 /* Options for korch_profile (reading A19). Zero-initialised fields take the defaults. */

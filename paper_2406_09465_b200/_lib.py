@@ -44,7 +44,7 @@ class KorchError(RuntimeError):
 
 class EnumOpts(C.Structure):
     _fields_ = [("max_prims", C.c_int32), ("keep_multi_linear", C.c_int32), ("max_states", C.c_int64),
-                ("partition_max", C.c_int32), ("attention_pairs", C.c_int32)]
+                ("partition_max", C.c_int32), ("attention_pairs", C.c_int32), ("max_outputs", C.c_int32)]
 
 
 class CandDesc(C.Structure):
@@ -52,7 +52,8 @@ class CandDesc(C.Structure):
                 ("n_inputs", C.c_int32), ("inputs", C.POINTER(C.c_int32)),
                 ("n_graph_inputs", C.c_int32), ("graph_inputs", C.POINTER(C.c_int32)),
                 ("klass", C.c_int32), ("n_dense_linear", C.c_int32), ("bytes", C.c_int64),
-                ("flops", C.c_double), ("signature", C.c_char_p), ("part", C.c_int32)]
+                ("flops", C.c_double), ("signature", C.c_char_p), ("part", C.c_int32),
+                ("n_extra_outputs", C.c_int32), ("extra_outputs", C.POINTER(C.c_int32))]
 
 
 class ProfOpts(C.Structure):

@@ -85,13 +85,42 @@ class KorchGraph:
 
     # ---------------------------------------------------------------- candidates
     def enumerate(self, max_prims: int = 16, keep_multi_linear: bool = False, max_states: int = 1_000_000,
-                  partition_max: int = 0, attention_pairs: bool = False):
-        o = _lib.EnumOpts(max_prims, int(keep_multi_linear), max_states, partition_max, int(attention_pairs))
+                  partition_max: int = 0, attention_pairs: bool = False, max_outputs: int = 1):
+        o = _lib.EnumOpts(max_prims, int(keep_multi_linear), max_states, partition_max, int(attention_pairs),
+                          int(max_outputs))
         nc, ns = C.c_int64(), C.c_int64()
         check(LIB.korch_enumerate(self.h, C.byref(o), C.byref(nc), C.byref(ns)))
         self.n_states = ns.value
         self.cands = [self.candidate(i) for i in range(nc.value)]
+        topo = self.topo_index()
+        for c in self.cands:
+            c["sink_topo"] = topo[c["output"]]   # the kernel's place in the schedule (A6)
         return self.cands
+
+    def topo_index(self):
+        """Position of every primitive in the library's topological order (Kahn, smallest
+        id first; the order kernels run in, reading A6)."""
+        import heapq
+        nodes = self.prim["nodes"]
+        preds = [sorted({r["node"] for r in nd["inputs"] if "node" in r}) for nd in nodes]
+        succ = [[] for _ in nodes]
+        for v, ps in enumerate(preds):
+            for u in ps:
+                succ[u].append(v)
+        indeg = [len(p) for p in preds]
+        ready = [v for v in range(len(nodes)) if not indeg[v]]
+        heapq.heapify(ready)
+        pos = [0] * len(nodes)
+        k = 0
+        while ready:
+            v = heapq.heappop(ready)
+            pos[v] = k
+            k += 1
+            for w in succ[v]:
+                indeg[w] -= 1
+                if not indeg[w]:
+                    heapq.heappush(ready, w)
+        return pos
 
     def candidate(self, i: int) -> dict:
         d = _lib.CandDesc()
@@ -100,6 +129,7 @@ class KorchGraph:
             "index": i,
             "members": [d.members[k] for k in range(d.n_members)],
             "output": d.output,
+            "extra_outputs": [d.extra_outputs[k] for k in range(d.n_extra_outputs)],
             "inputs": [d.inputs[k] for k in range(d.n_inputs)],
             "graph_inputs": [d.graph_inputs[k] for k in range(d.n_graph_inputs)],
             "klass": _lib.CLASS_NAMES[d.klass],

@@ -93,6 +93,9 @@ bool make_gemm_prologue(const Graph& g, const Candidate& c, int mm, const std::v
 KernelPlan generate_attention(const Graph& g, const Candidate& c);   // gemm_gen.cpp (N2)
 KernelPlan generate_gemm(const Graph& g, const Candidate& c);   // gemm_gen.cpp
 std::string kernel_prelude();
+// Kernel parameters of a candidate's secondary outputs (N1, reading A32): ", T* __restrict__
+// out1, ..." in the order of Candidate::extra_outputs, passed right after `out`.
+std::string extra_out_params(const Graph& g, const Candidate& c);
 std::string fmt_float(double v);
 uint64_t fnv1a(const std::string& s);
 

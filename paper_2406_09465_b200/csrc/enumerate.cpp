@@ -7,6 +7,7 @@
 // tensors of the topological order, parts grown greedily to `partition_max` primitives,
 // and Alg. 1 runs inside each part (a set inside one part is convex in G iff it is
 // convex in the part, since a path that leaves a part never returns).
+#include <functional>
 #include "enumerate.h"
 
 #include <algorithm>
@@ -232,10 +233,47 @@ std::vector<Candidate> enumerate_candidates(const Graph& g, const EnumOpts& o, i
   }
   if (n_states) *n_states = total_states;
   if (parts_out) *parts_out = parts;
+  // N1 ("for O in P'", P:352-360 possible output set; reading A32): every
+  // single-output candidate (P', o) also yields (P', o, E) for each non-empty E of at most
+  // max_outputs - 1 secondary outputs drawn from the members (other than o) that have a
+  // consumer outside P' or are graph outputs (A3), with the shape of o
+  if (o.max_outputs > 1) {
+    std::vector<char> is_out(n, 0);
+    for (int t : g.outputs) is_out[t] = 1;
+    const size_t n_single = out.size();
+    for (size_t ci = 0; ci < n_single; ++ci) {
+      std::vector<char> in_p(n, 0);
+      for (int v : out[ci].members) in_p[v] = 1;
+      std::vector<int> xs;
+      for (int u : out[ci].members) {
+        if (u == out[ci].output || g.prims[u].shape != g.prims[out[ci].output].shape) continue;
+        bool ext = is_out[u];
+        for (int w : g.succs[u]) ext = ext || !in_p[w];
+        if (ext) xs.push_back(u);
+      }
+      const int kmax = std::min<int>(o.max_outputs - 1, (int)xs.size());
+      std::vector<int> pick;
+      std::function<void(size_t)> rec = [&](size_t from) {
+        if (!pick.empty()) {
+          Candidate c = out[ci];
+          c.extra_outputs = pick;
+          out.push_back(std::move(c));
+        }
+        if ((int)pick.size() == kmax) return;
+        for (size_t i = from; i < xs.size(); ++i) {
+          pick.push_back(xs[i]);
+          rec(i + 1);
+          pick.pop_back();
+        }
+      };
+      rec(0);
+    }
+  }
   std::sort(out.begin(), out.end(), [](const Candidate& x, const Candidate& y) {
     if (x.output != y.output) return x.output < y.output;
     if (x.members.size() != y.members.size()) return x.members.size() < y.members.size();
-    return x.members < y.members;
+    if (x.members != y.members) return x.members < y.members;
+    return x.extra_outputs < y.extra_outputs;
   });
   return out;
 }

@@ -55,6 +55,7 @@ struct BitsHash {
 struct Candidate {
   std::vector<int> members;       // P', ascending
   int output = -1;                // o (unique sink, reading A4)
+  std::vector<int> extra_outputs; // E: secondary materialised outputs (N1, reading A32), ascending
   std::vector<int> inputs;        // primitive inputs (I row)
   std::vector<int> graph_inputs;  // graph-input indices read
   int klass = 0;                  // KORCH_CLASS_*
@@ -72,6 +73,7 @@ struct EnumOpts {
   int64_t max_states = 1000000;
   int partition_max = 0;          // > 0: partition into parts of about this many primitives
   bool attention_pairs = false;   // N2: keep MatMul pairs where the first feeds the second's A
+  int max_outputs = 1;            // N1: > 1 adds (P', o, E) with |E| <= max_outputs - 1 (reading A32)
 };
 
 // Reading A17: parts of the topological order separated at articulation tensors.

@@ -449,7 +449,7 @@ static KernelPlan generate_gather_gemm(const Graph& g, const Candidate& c, int m
     k << "extern \"C\" __global__ void __launch_bounds__(192, 1) KNAME(";
     for (size_t i = 0; i < kp.ext.size(); ++i)
       k << "const " << (g.dtype_of(kp.ext[i]) == DType::F32 ? "float" : "bf16_t") << "* __restrict__ p" << i << ", ";
-    k << (g.prims[c.output].dtype == DType::F32 ? "float" : "bf16_t") << "* __restrict__ out, "
+    k << (g.prims[c.output].dtype == DType::F32 ? "float" : "bf16_t") << "* __restrict__ out" << extra_out_params(g, c) << ", "
       << "const __grid_constant__ TmaMap tmA) {\n";
     k << "  typedef int idx_t;\n";
     k << "  extern __shared__ __align__(1024) unsigned char smem_raw[];\n";
@@ -700,7 +700,7 @@ static KernelPlan generate_prologue_gemm(const Graph& g, const Candidate& c, int
     k << "extern \"C\" __global__ void __launch_bounds__(192, 1) KNAME(";
     for (size_t i = 0; i < ep.ext.size(); ++i)
       k << "const " << (g.dtype_of(ep.ext[i]) == DType::F32 ? "float" : "bf16_t") << "* __restrict__ p" << i << ", ";
-    k << (g.prims[c.output].dtype == DType::F32 ? "float" : "bf16_t") << "* __restrict__ out, "
+    k << (g.prims[c.output].dtype == DType::F32 ? "float" : "bf16_t") << "* __restrict__ out" << extra_out_params(g, c) << ", "
       << "const __grid_constant__ TmaMap tmB" << (staged ? ", const __grid_constant__ TmaMap tmX" : "") << ") {\n";
     k << "  typedef " << (numel(C) >= (1LL << 31) ? "long long" : "int") << " idx_t;\n";
     k << "  extern __shared__ __align__(1024) unsigned char smem_raw[];\n";
@@ -1050,7 +1050,7 @@ KernelPlan generate_gemm(const Graph& g, const Candidate& c) {
       k << "extern \"C\" __global__ void __launch_bounds__(192, 1) KNAME(";
       for (size_t i = 0; i < kp.ext.size(); ++i)
         k << "const " << (g.dtype_of(kp.ext[i]) == DType::F32 ? "float" : "bf16_t") << "* __restrict__ p" << i << ", ";
-      k << (g.prims[c.output].dtype == DType::F32 ? "float" : "bf16_t") << "* __restrict__ out, ";
+      k << (g.prims[c.output].dtype == DType::F32 ? "float" : "bf16_t") << "* __restrict__ out" << extra_out_params(g, c) << ", ";
       k << "const __grid_constant__ TmaMap tmA, const __grid_constant__ TmaMap tmB) {\n";
       k << "  typedef int idx_t;\n";
       k << "  extern __shared__ __align__(1024) unsigned char smem_raw[];\n";
@@ -1241,7 +1241,7 @@ KernelPlan generate_gemm(const Graph& g, const Candidate& c) {
     k << "extern \"C\" __global__ void __launch_bounds__(128, 1) KNAME(";
     for (size_t i = 0; i < kp.ext.size(); ++i)
       k << "const " << (g.dtype_of(kp.ext[i]) == DType::F32 ? "float" : "bf16_t") << "* __restrict__ p" << i << ", ";
-    k << (g.prims[c.output].dtype == DType::F32 ? "float" : "bf16_t") << "* __restrict__ out, ";
+    k << (g.prims[c.output].dtype == DType::F32 ? "float" : "bf16_t") << "* __restrict__ out" << extra_out_params(g, c) << ", ";
     k << "const __grid_constant__ TmaMap tmA, const __grid_constant__ TmaMap tmB";
     for (size_t i = 0; i < sdesc.size(); ++i) k << ", const __grid_constant__ TmaMap tmS" << i;
     k << ") {\n";
@@ -1525,7 +1525,7 @@ KernelPlan generate_attention(const Graph& g, const Candidate& c) {
   k << "extern \"C\" __global__ void __launch_bounds__(192, 1) KNAME(";
   for (size_t i = 0; i < kp.ext.size(); ++i)
     k << "const " << (g.dtype_of(kp.ext[i]) == DType::F32 ? "float" : "bf16_t") << "* __restrict__ p" << i << ", ";
-  k << (g.prims[c.output].dtype == DType::F32 ? "float" : "bf16_t") << "* __restrict__ out, "
+  k << (g.prims[c.output].dtype == DType::F32 ? "float" : "bf16_t") << "* __restrict__ out" << extra_out_params(g, c) << ", "
     << "const __grid_constant__ TmaMap tmQ, const __grid_constant__ TmaMap tmK, const __grid_constant__ TmaMap tmV) {\n";
   k << "  typedef int idx_t;\n";
   k << "  extern __shared__ __align__(1024) unsigned char smem_raw[];\n";

@@ -121,7 +121,7 @@ struct Step {
   int cand = -1;
   int variant = 0;
   std::vector<BufRef> args;
-  BufRef out;
+  std::vector<BufRef> outs;  // the sink, then the secondary outputs (N1) in Candidate order
 };
 
 struct korch_graph {
@@ -433,19 +433,23 @@ static void encode_tma(const TmaDesc& d, const void* base, CUtensorMap* out) {
 }
 
 static void launch_variant(korch_ctx* ctx, const KernelPlan& plan, int vi, const std::vector<const void*>& ins,
-                           void* out, CUstream stream, bool pdl = false) {
+                           const std::vector<void*>& outs, CUstream stream, bool pdl = false) {
   const KernelVariant& v = plan.variants[vi];
   Module* m = ctx->module_for(v.name);
   CUfunction fn = load_fn(ctx, m, v);
-  std::vector<CUdeviceptr> ptrs(ins.size() + 1);
+  if (outs.empty()) throw KorchError(KORCH_E_ARG, "kernel launched without an output buffer");
+  void* out = outs[0];
+  std::vector<CUdeviceptr> ptrs(ins.size() + outs.size());
   std::vector<void*> args;
-  args.reserve(ins.size() + 1 + v.tma.size());
+  args.reserve(ins.size() + outs.size() + 1 + v.tma.size());
   for (size_t i = 0; i < ins.size(); ++i) {
     ptrs[i] = (CUdeviceptr)ins[i];
     args.push_back(&ptrs[i]);
   }
-  ptrs[ins.size()] = (CUdeviceptr)out;
-  args.push_back(&ptrs[ins.size()]);
+  for (size_t k = 0; k < outs.size(); ++k) {  // out, then the secondary outputs out1.. (N1)
+    ptrs[ins.size() + k] = (CUdeviceptr)outs[k];
+    args.push_back(&ptrs[ins.size() + k]);
+  }
   CUdeviceptr scratch = m->scratch;
   if (v.scratch_bytes > 0) {
     if (!scratch) throw KorchError(KORCH_E_CUDA, "kernel scratch not prepared: " + v.name);
@@ -609,6 +613,7 @@ korch_status korch_enumerate(korch_graph* G, const korch_enum_opts* o, int64_t* 
       if (o->max_states > 0) eo.max_states = o->max_states;
       if (o->partition_max > 0) eo.partition_max = o->partition_max;
       eo.attention_pairs = o->attention_pairs != 0;
+      if (o->max_outputs > 1) eo.max_outputs = std::min<int32_t>(o->max_outputs, 4);
     }
     std::lock_guard<std::mutex> lk(G->mu);
     G->cands = enumerate_candidates(G->g, eo, &G->n_states);
@@ -639,6 +644,8 @@ korch_status korch_candidate(const korch_graph* G, int64_t i, korch_cand_desc* d
   d->flops = c.flops;
   d->signature = c.signature.c_str();
   d->part = c.part;
+  d->n_extra_outputs = (int32_t)c.extra_outputs.size();
+  d->extra_outputs = c.extra_outputs.data();
   return KORCH_OK;
 }
 
@@ -753,8 +760,15 @@ korch_status korch_profile(korch_graph* G, const int64_t* idx, int64_t n, const 
         offs.push_back(tot);
         tot += ((size_t)tensor_bytes(G->g, r) + 255) & ~(size_t)255;
       }
-      size_t out_off = tot;
-      tot += ((size_t)tensor_bytes(G->g, Ref{false, G->cands[ci].output}) + 255) & ~(size_t)255;
+      std::vector<size_t> out_offs;
+      {
+        std::vector<int> os{G->cands[ci].output};
+        os.insert(os.end(), G->cands[ci].extra_outputs.begin(), G->cands[ci].extra_outputs.end());
+        for (int o : os) {
+          out_offs.push_back(tot);
+          tot += ((size_t)tensor_bytes(G->g, Ref{false, o}) + 255) & ~(size_t)255;
+        }
+      }
       CUdeviceptr base = ctx->arena_get(tot);
       std::vector<const void*> ins;
       for (size_t e = 0; e < s.plan.ext.size(); ++e) {
@@ -765,7 +779,8 @@ korch_status korch_profile(korch_graph* G, const int64_t* idx, int64_t n, const 
         else CU_CHECK(cu.cuMemsetD16Async(p, 0x3f80, ne, ctx->pstream));
         ins.push_back((const void*)p);
       }
-      void* outp = (void*)(base + out_off);
+      std::vector<void*> outp;
+      for (size_t oo : out_offs) outp.push_back((void*)(base + oo));
       int64_t best = INT64_MAX;
       int bestv = -1;
       if (tune || s.var_ns.size() != s.plan.variants.size()) s.var_ns.assign(s.plan.variants.size(), -1);
@@ -910,23 +925,31 @@ korch_status korch_set_orchestration(korch_graph* G, const int64_t* sel, int64_t
     std::vector<int64_t> order(sel, sel + n);
     for (auto i : order)
       if (i < 0 || i >= (int64_t)G->cands.size()) return fail(KORCH_E_ARG, "candidate index out of range");
-    // A6: order by topological index of the output, ties by candidate index
+    // A6: order by topological index of the output (the sink), ties by candidate index
     std::sort(order.begin(), order.end(), [&](int64_t a, int64_t b) {
       int ta = g.topo_index[G->cands[a].output], tb = g.topo_index[G->cands[b].output];
       return ta != tb ? ta < tb : a < b;
     });
+    auto outs_of = [&](int64_t i) {
+      std::vector<int> os{G->cands[i].output};
+      os.insert(os.end(), G->cands[i].extra_outputs.begin(), G->cands[i].extra_outputs.end());
+      return os;
+    };
     std::vector<int64_t> uniq;
-    std::vector<int> producer(g.prims.size(), -1);  // prim -> step index
+    std::vector<int> producer(g.prims.size(), -1);  // prim -> step index of its first producer
     for (auto i : order) {
-      int o = G->cands[i].output;
-      if (producer[o] >= 0) continue;  // A7: earliest producer binds
-      producer[o] = (int)uniq.size();
+      bool any_new = false;
+      for (int t : outs_of(i)) any_new = any_new || producer[t] < 0;
+      if (!any_new) continue;  // A7: every output already bound to an earlier producer
+      for (int t : outs_of(i))
+        if (producer[t] < 0) producer[t] = (int)uniq.size();
       uniq.push_back(i);
     }
-    // Eq. 4: every input of a kernel is produced by an earlier kernel
+    // Eq. 4 / Eq. 4' (reading A32): every input of a kernel is materialised by a selected
+    // kernel whose sink precedes its own; the first producer in order has the earliest sink
     for (size_t s = 0; s < uniq.size(); ++s)
       for (int p : G->cands[uniq[s]].inputs)
-        if (producer[p] < 0 || producer[p] >= (int)s)
+        if (producer[p] < 0 || g.topo_index[G->cands[uniq[producer[p]]].output] >= g.topo_index[G->cands[uniq[s]].output])
           return fail(KORCH_E_INFEASIBLE, "Eq. 4 violated: kernel " + std::to_string(uniq[s]) + " needs p" +
                                               std::to_string(p) + " which no earlier selected kernel produces");
     // Eq. 3: every output primitive is produced
@@ -994,16 +1017,30 @@ korch_status korch_set_orchestration(korch_graph* G, const int64_t* sel, int64_t
         else { b.kind = BufRef::Work; b.offset = off_of[r.id]; }
         st.args.push_back(b);
       }
-      int o = G->cands[ci].output;
-      if (out_index.count(o)) { st.out.kind = BufRef::Output; st.out.index = out_index[o]; }
-      else {
-        off_of[o] = alloc((size_t)tensor_bytes(g, Ref{false, o}));
-        st.out.kind = BufRef::Work;
-        st.out.offset = off_of[o];
+      std::vector<std::pair<size_t, size_t>> scratch;  // (offset, bytes) released after this step
+      for (int o : outs_of(ci)) {
+        BufRef b;
+        const size_t nb = (size_t)tensor_bytes(g, Ref{false, o});
+        if (producer[o] != (int)s) {
+          // a later producer of an already materialised tensor (A7) writes a dead copy
+          b.kind = BufRef::Work;
+          b.offset = alloc(nb);
+          scratch.push_back({b.offset, nb});
+        } else if (out_index.count(o)) {
+          b.kind = BufRef::Output;
+          b.index = out_index[o];
+        } else {
+          off_of[o] = alloc(nb);
+          b.kind = BufRef::Work;
+          b.offset = off_of[o];
+          if (last_use[o] <= (int)s) scratch.push_back({b.offset, nb});  // never read again
+        }
+        st.outs.push_back(b);
       }
       // free tensors whose last consumer is this step
       for (int p : G->cands[ci].inputs)
         if (last_use[p] == (int)s && !out_index.count(p)) release(off_of[p], (size_t)tensor_bytes(g, Ref{false, p}));
+      for (auto& sc : scratch) release(sc.first, sc.second);
       steps.push_back(st);
     }
     G->steps = steps;
@@ -1046,6 +1083,11 @@ korch_status korch_execute(korch_graph* G, const void* const* inputs, void* cons
       if (b.kind == BufRef::Output) return outputs[b.index];
       return static_cast<char*>(workspace) + b.offset;
     };
+    auto resolve_outs = [&](const Step& st) {
+      std::vector<void*> r;
+      for (auto& b : st.outs) r.push_back(resolve(b));
+      return r;
+    };
     static const bool direct = getenv("KORCH_EXEC_DIRECT") != nullptr;
     static const bool use_pdl = !(getenv("KORCH_PDL") && std::string(getenv("KORCH_PDL")) == "0");
     if (direct || !G->gexec || ptrs != G->cap_ptrs)
@@ -1054,7 +1096,7 @@ korch_status korch_execute(korch_graph* G, const void* const* inputs, void* cons
       for (auto& st : G->steps) {
         std::vector<const void*> ins;
         for (auto& a : st.args) ins.push_back(resolve(a));
-        launch_variant(ctx, G->cs[st.cand].plan, st.variant, ins, resolve(st.out), (CUstream)stream);
+        launch_variant(ctx, G->cs[st.cand].plan, st.variant, ins, resolve_outs(st), (CUstream)stream);
       }
       return KORCH_OK;
     }
@@ -1068,7 +1110,7 @@ korch_status korch_execute(korch_graph* G, const void* const* inputs, void* cons
           std::vector<const void*> ins;
           for (auto& a : st.args) ins.push_back(resolve(a));
           // every kernel after the first overlaps its prologue with its predecessor (PDL)
-          launch_variant(ctx, G->cs[st.cand].plan, st.variant, ins, resolve(st.out), ctx->pstream, use_pdl && k > 0);
+          launch_variant(ctx, G->cs[st.cand].plan, st.variant, ins, resolve_outs(st), ctx->pstream, use_pdl && k > 0);
         }
       } catch (...) {
         CUgraph tmp = nullptr;
@@ -1182,6 +1224,11 @@ korch_status korch_execute_host(korch_graph* G, const void* const* host_inputs, 
       if (b.kind == BufRef::Output) return direct_out[b.index] ? direct_out[b.index] : dev_outputs[b.index];
       return static_cast<char*>(workspace) + b.offset;
     };
+    auto resolve_outs = [&](const Step& st) {
+      std::vector<void*> r;
+      for (auto& b : st.outs) r.push_back(resolve(b));
+      return r;
+    };
     static const bool use_pdl = !(getenv("KORCH_PDL") && std::string(getenv("KORCH_PDL")) == "0");
     if (!G->gexec_host || ptrs != G->cap_ptrs_host) {
       for (auto& st : G->steps) prepare_variant(ctx, G->cs[st.cand].plan.variants[st.variant]);
@@ -1207,7 +1254,7 @@ korch_status korch_execute_host(korch_graph* G, const void* const* host_inputs, 
           // kernels fetch graph inputs (weights, residual tiles, a staged LayerNorm input)
           // before griddepcontrol.wait, and here the inputs are being written by the copy
           // kernels just launched, so the plan may only start once they have completed
-          launch_variant(ctx, G->cs[st.cand].plan, st.variant, ins, resolve(st.out), ctx->pstream, use_pdl && k > 0);
+          launch_variant(ctx, G->cs[st.cand].plan, st.variant, ins, resolve_outs(st), ctx->pstream, use_pdl && k > 0);
         }
         for (size_t j = 0; j < g.outputs.size(); ++j)
           if (host_outputs[j] && !direct_out[j]) {

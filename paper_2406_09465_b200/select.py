@@ -6,8 +6,11 @@ candidates and costs, this module picks u, and korch_set_orchestration accepts i
   minimise   sum_i c_i u_i                                  (Eq. 2)
   s.t.       sum_i O_ij u_i >= 1          for p_j in T       (Eq. 3)
              sum_i O_ij u_i >= I_kj u_k   for all j, k       (Eq. 4)
-with O_ij = 1 iff p_j is the materialised output of K_i (reading A2) and I_kj = 1
-iff p_j is an input of K_k.  Solved with HiGHS (scipy.optimize.milp) in place of
+with O_ij = 1 iff p_j is a materialised output of K_i (reading A2; the sink, plus the
+secondary outputs of a multi-output candidate, N1 / reading A32) and I_kj = 1 iff p_j
+is an input of K_k.  With secondary outputs Eq. 4 becomes Eq. 4' (reading A32): the
+producers counted for an input of K_k are those whose sink precedes K_k's sink (kernels
+run in sink order, A6), which for single-output candidates is Eq. 4 unchanged.  Solved with HiGHS (scipy.optimize.milp) in place of
 PuLP/CBC (not installed).  Costs are integer nanoseconds; the objective
 c_i*(M+1) + 1 breaks ties toward fewer kernels (reading A8).
 """
@@ -100,6 +103,11 @@ LAST_EXPANDED = 0  # A* states expanded by the last solve (all parts)
 LAST_SOLVER = ""   # "exact" (native A*) or "highs" for the last solve
 
 
+def outputs_of(c):
+    """Materialised tensors of a candidate: the sink, then its secondary outputs (N1)."""
+    return [c["output"]] + list(c.get("extra_outputs", ()))
+
+
 def prune_dominated(cands, costs, live):
     """Exact reduction of the BLP before the MILP.
 
@@ -116,24 +124,64 @@ def prune_dominated(cands, costs, live):
         by_out.setdefault(cands[i]["output"], []).append(i)
     keep = []
     for o, group in by_out.items():
-        group.sort(key=lambda i: (costs[i], len(cands[i]["inputs"]), i))
+        # same sink (so the same place in the schedule, Eq. 4'); j dominates i when it
+        # materialises a superset of i's outputs from a subset of its inputs at no more cost
+        group.sort(key=lambda i: (costs[i], len(cands[i]["inputs"]), -len(outputs_of(cands[i])), i))
         kept = []
         for i in group:
             ins = frozenset(cands[i]["inputs"])
-            if any(costs[j] <= costs[i] and ins_j <= ins for j, ins_j in kept):
+            outs = frozenset(outputs_of(cands[i]))
+            if any(costs[j] <= costs[i] and ins_j <= ins and outs <= outs_j for j, ins_j, outs_j in kept):
                 continue
-            kept.append((i, ins))
-        keep.extend(i for i, _ in kept)
+            kept.append((i, ins, outs))
+        keep.extend(i for i, _, _ in kept)
     alive = set(keep)
+    topo = _sink_rank(cands, live)
     changed = True
     while changed:
         changed = False
-        produced = {cands[i]["output"] for i in alive}
+        # earliest sink rank at which each tensor is materialised by a live candidate
+        first = {}
+        for i in alive:
+            for t in outputs_of(cands[i]):
+                first[t] = min(first.get(t, 1 << 60), topo[cands[i]["output"]])
         for i in list(alive):
-            if any(j not in produced for j in cands[i]["inputs"]):
+            if any(first.get(j, 1 << 60) >= topo[cands[i]["output"]] for j in cands[i]["inputs"]):
                 alive.discard(i)
                 changed = True
     return sorted(alive)
+
+
+def _sink_rank(cands, live):
+    """Schedule position of every live candidate's sink (reading A6): the library's
+    topological index ("sink_topo", set by KorchGraph.enumerate).  Without it (host tests
+    with hand-made single-output candidates) any topological rank of the sinks gives the
+    same Eq. 4; secondary outputs need the library's order, so it is then required."""
+    if all("sink_topo" in cands[i] for i in live):
+        return {cands[i]["output"]: cands[i]["sink_topo"] for i in live}
+    if any(cands[i].get("extra_outputs") for i in live):
+        raise ValueError("multi-output candidates need their sink's topological index ('sink_topo')")
+    import heapq
+    nodes, succ, indeg = set(), {}, {}
+    for i in live:
+        o = cands[i]["output"]
+        nodes.add(o)
+        for j in cands[i]["inputs"]:
+            nodes.add(j)
+            if o not in succ.setdefault(j, set()):
+                succ[j].add(o)
+                indeg[o] = indeg.get(o, 0) + 1
+    ready = [t for t in nodes if indeg.get(t, 0) == 0]
+    heapq.heapify(ready)
+    rank = {}
+    while ready:
+        t = heapq.heappop(ready)
+        rank[t] = len(rank)
+        for w in succ.get(t, ()):
+            indeg[w] -= 1
+            if indeg[w] == 0:
+                heapq.heappush(ready, w)
+    return rank
 
 
 def solve_blp(cands, costs, outputs, time_limit=600.0, exact=True, exact_time_limit=120.0):
@@ -145,9 +193,12 @@ def solve_blp(cands, costs, outputs, time_limit=600.0, exact=True, exact_time_li
     global LAST_OPTIMAL, LAST_GAP, LAST_SOLVER
     live = prune_dominated(cands, costs, [i for i, c in enumerate(costs) if c < INF])
     for t in outputs:
-        if not any(cands[i]["output"] == t for i in live):
+        if not any(t in outputs_of(cands[i]) for i in live):
             raise ValueError(f"infeasible: output p{t} has no generable producer")
-    if exact:
+    multi = any(cands[i].get("extra_outputs") for i in live)
+    # the native A* search resolves one producer per tensor (single-output candidates);
+    # with secondary outputs the MILP with Eq. 4' is solved instead (to optimality)
+    if exact and not multi:
         r = solve_exact(cands, costs, outputs, live, time_limit=min(time_limit, exact_time_limit))
         if r is not None:
             LAST_SOLVER = "exact" if LAST_SOLVER in ("", "exact") else "mixed"
@@ -157,7 +208,10 @@ def solve_blp(cands, costs, outputs, time_limit=600.0, exact=True, exact_time_li
     m = len(live)
     producers = {}
     for i in live:
-        producers.setdefault(cands[i]["output"], []).append(idx[i])
+        for t in outputs_of(cands[i]):
+            producers.setdefault(t, []).append(idx[i])
+    rank = _sink_rank(cands, live)
+    pos = {i: rank[cands[i]["output"]] for i in live}
     rows, cols, vals, lb = [], [], [], []
     r = 0
     for t in outputs:                                          # Eq. 3
@@ -168,10 +222,10 @@ def solve_blp(cands, costs, outputs, time_limit=600.0, exact=True, exact_time_li
             rows.append(r); cols.append(k); vals.append(1.0)
         lb.append(1.0)
         r += 1
-    for i in live:                                             # Eq. 4
+    for i in live:                                             # Eq. 4 (Eq. 4')
         k = idx[i]
         for j in cands[i]["inputs"]:
-            ps = producers.get(j, [])
+            ps = [p for p in producers.get(j, []) if pos[live[p]] < pos[i]]
             for p in ps:
                 rows.append(r); cols.append(p); vals.append(1.0)
             rows.append(r); cols.append(k); vals.append(-1.0)
@@ -181,7 +235,7 @@ def solve_blp(cands, costs, outputs, time_limit=600.0, exact=True, exact_time_li
     # A8 tie-break toward fewer kernels: an optimal selection has at most one producer per
     # tensor (A7), so it has at most (#distinct outputs) kernels and a weight of that + 1
     # per ns keeps any 1 ns difference in sum(c) above every kernel-count difference
-    w = float(len({cands[i]["output"] for i in live}) + 1)
+    w = float(len({t for i in live for t in outputs_of(cands[i])}) + 1)
     c = np.array([float(costs[i]) * w + 1.0 for i in live])
     res = milp(c, integrality=np.ones(m), bounds=Bounds(0, 1),
                constraints=LinearConstraint(a, np.array(lb), np.inf),
@@ -239,7 +293,7 @@ def operator_aligned(cands, prim_graph):
     by_op = {}
     for n in prim_graph["nodes"]:
         by_op.setdefault(n["op"], []).append(n["id"])
-    key = {tuple(c["members"]): i for i, c in enumerate(cands)}
+    key = {tuple(c["members"]): i for i, c in enumerate(cands) if not c.get("extra_outputs")}
     sel = []
     for op, members in sorted(by_op.items()):
         i = key.get(tuple(sorted(members)))
@@ -251,5 +305,5 @@ def operator_aligned(cands, prim_graph):
 
 def singletons(cands, n_prims):
     """One kernel per primitive (the fully unfused orchestration)."""
-    key = {tuple(c["members"]): i for i, c in enumerate(cands)}
+    key = {tuple(c["members"]): i for i, c in enumerate(cands) if not c.get("extra_outputs")}
     return sorted(key[(p,)] for p in range(n_prims))

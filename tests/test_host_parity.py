@@ -305,3 +305,53 @@ def test_blp_with_rejections_and_baselines(ctx):
     assert len(base) == len(g["nodes"])
     singles = kg.singletons()
     assert len(singles) == kg.n_prims
+
+
+# ------------------------------------------------------------------ N1 multi-output
+@pytest.mark.parametrize("name", ["c1", "c1_noaffine", "c2_b2", "misc", "cnn"])
+@pytest.mark.parametrize("max_outputs", [2, 3])
+def test_multi_output_enumeration_matches_oracle(ctx, name, max_outputs):
+    """N1 (reading A32): the library's (P', o, E) list equals the oracle's, in order."""
+    from oracle.multi_output import multi_output_candidates
+    g = GRAPHS[name]()
+    kg = KorchGraph(ctx, g)
+    ours = kg.enumerate(max_outputs=max_outputs)
+    G, ref = _oracle_cands(g)
+    want = multi_output_candidates(G, ref, max_outputs)
+    assert len(want) > len(ref)
+    assert [(tuple(c["members"]), c["output"], tuple(c["extra_outputs"])) for c in ours] == want
+    for c in ours:
+        assert c["inputs"] == candidate_inputs(G, c["members"])
+
+
+def test_multi_output_random_graphs(ctx):
+    from oracle.multi_output import multi_output_candidates
+    rng = np.random.default_rng(9)
+    for _ in range(20):
+        g = _random_op_graph(rng, int(rng.integers(2, 7)))
+        kg = KorchGraph(ctx, g)
+        ours = kg.enumerate(max_prims=8, max_outputs=2)
+        G, ref = _oracle_cands(g, max_prims=8)
+        assert [(tuple(c["members"]), c["output"], tuple(c["extra_outputs"])) for c in ours] == \
+            multi_output_candidates(G, ref, 2)
+
+
+def test_multi_output_blp_equals_oracle_search_c1(ctx):
+    """The product's selection (MILP with Eq. 4') reaches exactly the oracle's
+    producer-assignment optimum on C1 with multi-output candidates and seeded costs."""
+    from oracle.multi_output import feasible_mo, multi_output_candidates, producer_search_mo
+    g = c1_softmax_layernorm()
+    kg = KorchGraph(ctx, g)
+    cands = kg.enumerate(max_outputs=2)
+    G, ref = _oracle_cands(g)
+    mo = multi_output_candidates(G, ref, 2)
+    cin = [candidate_inputs(G, c[0]) for c in mo]
+    rng = np.random.default_rng(17)
+    for trial in range(4):
+        costs = [int(rng.integers(500, 5000)) for _ in mo]
+        costs = [c // 2 if mo[i][2] else c for i, c in enumerate(costs)]
+        want, wsel = producer_search_mo(mo, costs, G.outputs, cin, G.topo_index)
+        obj, sel = solve_blp(cands, costs, kg.outputs)
+        assert obj == want
+        assert feasible_mo(mo, sel, sorted(G.outputs), cin, G.topo_index)
+        kg.set_orchestration(sel)          # the library accepts it (Eq. 3 / Eq. 4')
