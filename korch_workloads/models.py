@@ -26,23 +26,23 @@ class _M:
         self.b = GraphBuilder(dtype)
         self.n = 0
 
-    def w(self, shape, std=None, mean=0.0):
+    def w(self, shape, std=None, mean=0.0, suffix=""):
         self.n += 1
         fan_in = 1
         for d in shape[1:] if len(shape) > 1 else shape:
             fan_in *= d
         if std is None:
             std = 1.0 / math.sqrt(max(1, fan_in))
-        return self.b.input(f"w{self.n}", shape, mean=mean, std=std)
+        return self.b.input(f"w{self.n}{suffix}", shape, mean=mean, std=std)
 
     def op(self, *a, **k):
         return self.b.op(*a, **k)
 
 
 # ---------------------------------------------------------------------------------- Candy
-def candy(size: int = 224, dtype: str = "bf16", blocks: int = 5):
+def candy(size: int = 224, dtype: str = "bf16", blocks: int = 5, batch: int = 1):
     m = _M(dtype)
-    x = m.b.input("x", [1, 3, size, size])
+    x = m.b.input("x", [batch, 3, size, size])
 
     def conv_layer(h, cin, cout, k, stride):
         p = k // 2
@@ -75,9 +75,10 @@ def candy(size: int = 224, dtype: str = "bf16", blocks: int = 5):
 
 # ------------------------------------------------------------------------------ SegFormer
 def segformer(size: int = 512, dtype: str = "bf16", dims=(32, 64, 160, 256), heads=(1, 2, 5, 8),
-              srs=(8, 4, 2, 1), depths=(2, 2, 2, 2), mlp=4, decoder=256, classes=150):
+              srs=(8, 4, 2, 1), depths=(2, 2, 2, 2), mlp=4, decoder=256, classes=150, batch: int = 1):
     m = _M(dtype)
-    x = m.b.input("x", [1, 3, size, size])
+    nb = batch
+    x = m.b.input("x", [nb, 3, size, size])
     eps = 1e-6
 
     def ln(t, c):
@@ -90,13 +91,13 @@ def segformer(size: int = 512, dtype: str = "bf16", dims=(32, 64, 160, 256), hea
         b = m.w([cout], std=0.02)
         return m.op("Add", m.op("MatMul", t, w), b)
 
-    def to_tokens(t, c, h, w):          # [1,C,H,W] -> [1,HW,C]
-        t = m.op("Reshape", t, shape=[1, c, h * w])
+    def to_tokens(t, c, h, w):          # [N,C,H,W] -> [N,HW,C]
+        t = m.op("Reshape", t, shape=[nb, c, h * w])
         return m.op("Transpose", t, perm=[0, 2, 1])
 
-    def to_nchw(t, c, h, w):            # [1,HW,C] -> [1,C,H,W]
+    def to_nchw(t, c, h, w):            # [N,HW,C] -> [N,C,H,W]
         t = m.op("Transpose", t, perm=[0, 2, 1])
-        return m.op("Reshape", t, shape=[1, c, h, w])
+        return m.op("Reshape", t, shape=[nb, c, h, w])
 
     feats = []
     cur, cin, hw = x, 3, size
@@ -123,15 +124,15 @@ def segformer(size: int = 512, dtype: str = "bf16", dims=(32, 64, 160, 256), hea
             else:
                 kvx, nr = y, n
             kv = linear(kvx, c, 2 * c)
-            qh = m.op("Transpose", m.op("Reshape", q, shape=[1, n, nh, d]), perm=[0, 2, 1, 3])
+            qh = m.op("Transpose", m.op("Reshape", q, shape=[nb, n, nh, d]), perm=[0, 2, 1, 3])
             kk = m.op("Slice", kv, axis=2, start=0, end=c)
             vv = m.op("Slice", kv, axis=2, start=c, end=2 * c)
-            kt = m.op("Transpose", m.op("Reshape", kk, shape=[1, nr, nh, d]), perm=[0, 2, 3, 1])
-            vh = m.op("Transpose", m.op("Reshape", vv, shape=[1, nr, nh, d]), perm=[0, 2, 1, 3])
+            kt = m.op("Transpose", m.op("Reshape", kk, shape=[nb, nr, nh, d]), perm=[0, 2, 3, 1])
+            vh = m.op("Transpose", m.op("Reshape", vv, shape=[nb, nr, nh, d]), perm=[0, 2, 1, 3])
             sc = m.op("DivC", m.op("MatMul", qh, kt), c=math.sqrt(d))
             p = m.op("Softmax", sc, axis=3)
             o = m.op("MatMul", p, vh)
-            o = m.op("Reshape", m.op("Transpose", o, perm=[0, 2, 1, 3]), shape=[1, n, c])
+            o = m.op("Reshape", m.op("Transpose", o, perm=[0, 2, 1, 3]), shape=[nb, n, c])
             t = m.op("Add", t, linear(o, c, c))
             # Mix-FFN: fc1 -> 3x3 depthwise conv -> GELU -> fc2
             y = ln(t, c)
@@ -149,13 +150,13 @@ def segformer(size: int = 512, dtype: str = "bf16", dims=(32, 64, 160, 256), hea
     top = feats[0][2]
     ups = []
     for (t, c, hw) in reversed(feats):
-        u = linear(t, c, decoder)                                 # [1, hw*hw, D]
+        u = linear(t, c, decoder)                                 # [N, hw*hw, D]
         f = top // hw
         if f > 1:                                                 # nearest x f in NHWC tokens
-            u = m.op("Reshape", u, shape=[1, hw, hw, decoder])
+            u = m.op("Reshape", u, shape=[nb, hw, hw, decoder])
             u = m.op("Broadcast", u, axis=2, size=f)
             u = m.op("Broadcast", u, axis=4, size=f)
-            u = m.op("Reshape", u, shape=[1, top * top, decoder])
+            u = m.op("Reshape", u, shape=[nb, top * top, decoder])
         ups.append(u)
     u = m.op("Concat", *ups, axis=2)                              # [1, top^2, 4D]
     u = m.op("Relu", linear(u, 4 * decoder, decoder))             # linear_fuse (+folded BN) + ReLU
@@ -166,13 +167,15 @@ def segformer(size: int = 512, dtype: str = "bf16", dims=(32, 64, 160, 256), hea
 
 # --------------------------------------------------------------------------- EfficientViT
 def efficientvit(size: int = 224, dtype: str = "bf16", widths=(16, 32, 64, 128, 256), depths=(1, 2, 3, 3, 4),
-                 dim: int = 16, expand: int = 4, eps: float = 1e-15):
+                 dim: int = 16, expand: int = 4, eps: float = 1e-15, batch: int = 1):
     """EfficientViT-B1 backbone: conv stem + DSConv, MBConv
     stages, then EfficientViT blocks (LiteMLA ReLU linear attention with 5x5 multi-scale
     aggregation + MBConv).  Hardswish activations, BN folded.  Pointwise (1x1) convs are
-    MatMuls over [C, HW] (tcgen05 GEMMs); depthwise / strided convs stay Conv."""
+    MatMuls over [C, HW] (tcgen05 GEMMs); depthwise / strided convs stay Conv.  At batch
+    N > 1 a pointwise conv is the token-major MatMul [N, HW, Cin] x W^T (see _pw)."""
     m = _M(dtype)
-    x = m.b.input("x", [1, 3, size, size])
+    nb = batch
+    x = m.b.input("x", [nb, 3, size, size])
 
     def conv(h, cin, cout, k, stride=1, groups=1, bias=True):
         w = m.w([cout, cin // groups, k, k])
@@ -180,6 +183,8 @@ def efficientvit(size: int = 224, dtype: str = "bf16", widths=(16, 32, 64, 128, 
         return m.op("Conv", *args, stride=[stride, stride], pads=[k // 2, k // 2], groups=groups)
 
     def pw(h, cin, cout, hw, bias=True):             # 1x1 conv as MatMul on [C, HW]
+        if nb > 1:
+            return _pw(m, h, nb, cin, cout, hw, bias)
         t = m.op("Reshape", h, shape=[cin, hw * hw])
         t = m.op("MatMul", m.w([cout, cin]), t)
         if bias:
@@ -201,7 +206,7 @@ def efficientvit(size: int = 224, dtype: str = "bf16", widths=(16, 32, 64, 128, 
         agg = conv(qkv, 3 * c, 3 * c, 5, groups=3 * c, bias=False)                   # 5x5 depthwise
         agg = conv(agg, 3 * c, 3 * c, 1, groups=3 * heads, bias=False)               # grouped 1x1
         ms = m.op("Concat", qkv, agg, axis=1)                                        # [1,6c,hw,hw]
-        ms = m.op("Reshape", ms, shape=[1, 2 * heads, 3 * dim, n])
+        ms = m.op("Reshape", ms, shape=[nb, 2 * heads, 3 * dim, n])
         ms = m.op("Transpose", ms, perm=[0, 1, 3, 2])                                # [1,2h,n,3d]
         q = m.op("Relu", m.op("Slice", ms, axis=3, start=0, end=dim))
         k = m.op("Relu", m.op("Slice", ms, axis=3, start=dim, end=2 * dim))
@@ -212,10 +217,10 @@ def efficientvit(size: int = 224, dtype: str = "bf16", widths=(16, 32, 64, 128, 
         o = m.op("MatMul", q, kv)                                                    # [1,2h,n,d+1]
         num = m.op("Slice", o, axis=3, start=0, end=dim)
         den = m.op("AddC", m.op("Slice", o, axis=3, start=dim, end=dim + 1), c=eps)
-        den = m.op("Reshape", den, shape=[1, 2 * heads, n])
+        den = m.op("Reshape", den, shape=[nb, 2 * heads, n])
         o = m.op("Div", num, m.op("Broadcast", den, axis=3, size=dim))
         o = m.op("Transpose", o, perm=[0, 1, 3, 2])                                  # [1,2h,d,n]
-        o = m.op("Reshape", o, shape=[1, 2 * c, hw, hw])
+        o = m.op("Reshape", o, shape=[nb, 2 * c, hw, hw])
         return pw(o, 2 * c, c, hw)
 
     h = m.op("HardSwish", conv(x, 3, widths[0], 3, 2))
@@ -241,20 +246,24 @@ def efficientvit(size: int = 224, dtype: str = "bf16", widths=(16, 32, 64, 128, 
 
 
 # ----------------------------------------------------------------------------- YOLOX-Nano
-def yolox_nano(size: int = 416, dtype: str = "bf16", width: float = 0.25, classes: int = 80):
+def yolox_nano(size: int = 416, dtype: str = "bf16", width: float = 0.25, classes: int = 80, batch: int = 1):
     """YOLOX-Nano: Focus, depthwise CSPDarknet (depth 0.33,
     width 0.25), SPP 5/9/13, PAFPN, decoupled heads; SiLU, BN folded.  Output
     [1, 3549, 85] at 416^2 = cat(reg, sigmoid(obj), sigmoid(cls)) per anchor point (the box
     decode with grids / strides is not part of the graph).  1x1 convs are MatMuls over
-    [C, HW]; depthwise and 3x3 convs stay Conv."""
+    [C, HW]; depthwise and 3x3 convs stay Conv.  At batch N > 1 a pointwise conv is the
+    token-major MatMul [N, HW, Cin] x W^T (see _pw) and the output is [N, 3549, 85]."""
     m = _M(dtype)
-    x = m.b.input("x", [1, 3, size, size])
+    nb = batch
+    x = m.b.input("x", [nb, 3, size, size])
     c0 = int(64 * width)
 
     def silu(h):
         return m.op("SiLU", h)
 
     def pw(h, cin, cout, hw):                       # BaseConv 1x1 + SiLU as a MatMul
+        if nb > 1:
+            return silu(_pw(m, h, nb, cin, cout, hw, True))
         t = m.op("Reshape", h, shape=[cin, hw * hw])
         t = m.op("Add", m.op("MatMul", m.w([cout, cin]), t), m.w([cout, 1], std=0.02))
         return silu(m.op("Reshape", t, shape=[1, cout, hw, hw]))
@@ -280,9 +289,9 @@ def yolox_nano(size: int = 416, dtype: str = "bf16", width: float = 0.25, classe
 
     # Focus: space-to-depth, channel order (w-parity, h-parity, c)
     hw = size // 2
-    f = m.op("Reshape", x, shape=[1, 3, hw, 2, hw, 2])
+    f = m.op("Reshape", x, shape=[nb, 3, hw, 2, hw, 2])
     f = m.op("Transpose", f, perm=[0, 5, 3, 1, 2, 4])
-    f = m.op("Reshape", f, shape=[1, 12, hw, hw])
+    f = m.op("Reshape", f, shape=[nb, 12, hw, hw])
     h = conv(f, 12, c0, 3, 1)
     h, hw = dwconv(h, c0, 2 * c0, hw, 2)
     h = csp(h, 2 * c0, 2 * c0, hw, 1)
@@ -316,15 +325,41 @@ def yolox_nano(size: int = 416, dtype: str = "bf16", width: float = 0.25, classe
         r, _ = dwconv(st, hid, hid, s)
         r, _ = dwconv(r, hid, hid, s)
 
+        if nb > 1:
+            def pred(t, cout):                                                   # [N, s*s, cout]
+                return _pw(m, t, nb, hid, cout, s, True, tokens_out=True)
+            o = m.op("Concat", pred(r, 4), m.op("Sigmoid", pred(r, 1)), m.op("Sigmoid", pred(c, classes)), axis=2)
+            outs.append(o)                                                       # [N, s*s, 85]
+            continue
+
         def pred(t, cout):
             t2 = m.op("Reshape", t, shape=[hid, s * s])
             return m.op("Add", m.op("MatMul", m.w([cout, hid]), t2), m.w([cout, 1], std=0.02))   # [cout, s*s]
         o = m.op("Concat", pred(r, 4), m.op("Sigmoid", pred(r, 1)), m.op("Sigmoid", pred(c, classes)), axis=0)
         outs.append(o)                                                                           # [85, s*s]
+    if nb > 1:
+        m.b.output(m.op("Concat", *outs, axis=1))                                                # [N, 3549, 85]
+        return m.b.build()
     o = m.op("Concat", *outs, axis=1)                                                            # [85, 3549]
     o = m.op("Transpose", o, perm=[1, 0])
     m.b.output(m.op("Reshape", o, shape=[1, o_n(size), 5 + classes]))
     return m.b.build()
+
+
+def _pw(m, h, nb, cin, cout, hw, bias, tokens_out=False):
+    """Batched pointwise (1x1) convolution on [N, Cin, H, W] as a token-major MatMul:
+    [N, HW, Cin] x W^T[Cin, Cout] (+ bias) -> [N, Cout, H, W] (or the [N, HW, Cout] tokens).
+    MatMul broadcasts a 2-D B over the batch (ONNX semantics); the transposes are layout
+    primitives the GEMM template folds into its operand views / store addresses."""
+    t = m.op("Reshape", h, shape=[nb, cin, hw * hw])
+    t = m.op("Transpose", t, perm=[0, 2, 1])
+    t = m.op("MatMul", t, m.w([cin, cout], std=1.0 / math.sqrt(cin), suffix="T"))   # W^T of the batch-1 graph
+    if bias:
+        t = m.op("Add", t, m.w([cout], std=0.02))
+    if tokens_out:
+        return t
+    t = m.op("Transpose", t, perm=[0, 2, 1])
+    return m.op("Reshape", t, shape=[nb, cout, hw, hw])
 
 
 def o_n(size):
@@ -333,4 +368,4 @@ def o_n(size):
 
 MODELS = {"candy": candy, "segformer": segformer, "efficientvit": efficientvit, "yolox": yolox_nano,
           # the paper's EfficientViT resolution (reading A22), 1024:1 K^T V at stage 3
-          "efficientvit2048": lambda: efficientvit(size=2048)}
+          "efficientvit2048": lambda batch=1: efficientvit(size=2048, batch=batch)}
