@@ -495,6 +495,51 @@ static void launch_variant(korch_ctx* ctx, const KernelPlan& plan, int vi, const
 
 static int64_t tensor_bytes(const Graph& g, const Ref& r) { return numel(g.shape_of(r)) * dtype_size(g.dtype_of(r)); }
 
+// Seeded synthetic operands for the profiler ("allocate seeded inputs
+// at the candidate's exact shapes"): element i of a buffer with seed s is
+// u = hash(s, i) / 2^32 mapped to [-1, 1), stored as f32 or bf16 (round to nearest even).
+// A counter-based hash, so every buffer is reproducible and no host data is uploaded.
+static const KernelVariant& fill_variant() {
+  static KernelVariant v = [] {
+    KernelVariant k;
+    k.name = "korch_fill_v1";
+    k.block = 256;
+    k.source =
+        "KI unsigned korch_hash(unsigned s, unsigned long long i) {\n"
+        "  unsigned long long z = i * 0x9E3779B97F4A7C15ull + ((unsigned long long)s << 32) + s;\n"
+        "  z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull; z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;\n"
+        "  return (unsigned)((z ^ (z >> 31)) >> 32);\n}\n"
+        "KI float korch_u11(unsigned h) { return (float)(h >> 8) * (1.0f / 8388608.0f) - 1.0f; }\n"
+        "extern \"C\" __global__ void __launch_bounds__(256) korch_fill_v1(unsigned* __restrict__ dst, "
+        "unsigned long long nwords, unsigned seed, int bf16) {\n"
+        "  for (unsigned long long w = blockIdx.x * 256ull + threadIdx.x; w < nwords; w += gridDim.x * 256ull) {\n"
+        "    if (bf16) dst[w] = pack2(korch_u11(korch_hash(seed, 2 * w)), korch_u11(korch_hash(seed, 2 * w + 1)));\n"
+        "    else dst[w] = __float_as_uint(korch_u11(korch_hash(seed, w)));\n"
+        "  }\n}\n";
+    return k;
+  }();
+  return v;
+}
+
+static void prepare_fill(korch_ctx* ctx) {
+  const KernelVariant& v = fill_variant();
+  Module* m = ctx->module_for(v.name);
+  if (!m->compiled && !m->failed) compile_batch({{m, &v}}, default_cache_dir());
+  if (!m->compiled) throw KorchError(KORCH_E_NVRTC, "profiler fill kernel: " + m->log);
+  load_fn(ctx, m, v);
+}
+
+// fill `elems` elements of dtype `dt` at `p` (the buffer is 256-byte padded, so the last
+// bf16 word may cover one padding element)
+static void launch_fill(korch_ctx* ctx, CUdeviceptr p, size_t elems, DType dt, unsigned seed, CUstream stream) {
+  Module* m = ctx->module_for(fill_variant().name);
+  const int bf = dt == DType::BF16;
+  unsigned long long nwords = bf ? (elems + 1) / 2 : elems;
+  unsigned grid = (unsigned)std::max<unsigned long long>(1, std::min<unsigned long long>(8 * 148, (nwords + 255) / 256));
+  void* args[] = {&p, &nwords, &seed, (void*)&bf};
+  CU_CHECK(cuda().cuLaunchKernel(m->fn, grid, 1, 1, 256, 1, 1, 0, stream, args, nullptr));
+}
+
 // ------------------------------------------------------------------ API
 extern "C" {
 
@@ -713,6 +758,7 @@ korch_status korch_profile(korch_graph* G, const int64_t* idx, int64_t n, const 
       if (r != CUDA_SUCCESS) throw KorchError(KORCH_E_OOM, "flush buffer: " + cu_err(r));
     }
     CUevent e0, e1;
+    prepare_fill(ctx);
     CU_CHECK(cu.cuEventCreate(&e0, CU_EVENT_DEFAULT));
     CU_CHECK(cu.cuEventCreate(&e1, CU_EVENT_DEFAULT));
     for (int64_t k = 0; k < n; ++k) {
@@ -775,8 +821,7 @@ korch_status korch_profile(korch_graph* G, const int64_t* idx, int64_t n, const 
         const Ref& r = s.plan.ext[e];
         CUdeviceptr p = base + offs[e];
         size_t ne = (size_t)numel(G->g.shape_of(r));
-        if (G->g.dtype_of(r) == DType::F32) CU_CHECK(cu.cuMemsetD32Async(p, 0x3f800000u, ne, ctx->pstream));
-        else CU_CHECK(cu.cuMemsetD16Async(p, 0x3f80, ne, ctx->pstream));
+        launch_fill(ctx, p, ne, G->g.dtype_of(r), (unsigned)(e + 1), ctx->pstream);
         ins.push_back((const void*)p);
       }
       std::vector<void*> outp;

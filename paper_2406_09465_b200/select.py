@@ -307,3 +307,73 @@ def singletons(cands, n_prims):
     """One kernel per primitive (the fully unfused orchestration)."""
     key = {tuple(c["members"]): i for i, c in enumerate(cands) if not c.get("extra_outputs")}
     return sorted(key[(p,)] for p in range(n_prims))
+
+
+def greedy_fusion(cands, costs, prim_graph, outputs):
+    """Fission followed by greedy fusion, without the BLP: the ablation of P:505-518 (the
+    paper feeds the fissioned primitive graph to TensorRT and lets it pick the kernels) and
+    the 'always fuse what can be fused' policy of P:611-616 (TVM fuses the whole
+    memory-bound subgraph).  Start from one kernel per primitive; walk the primitives in
+    topological order and merge a primitive's kernel into its consumer's when the consumer
+    kernel is that kernel's only consumer and the union is a generable candidate (same
+    templates, cost < inf).  Primitives are visited consumers first (reverse topological
+    order) so producers join the kernel their consumers already formed (TVM's
+    producer-into-consumer fusion).  Every kernel materialises its sink; the result is a
+    partition (no redundant computation).  Returns the selection (sorted candidate indices)."""
+    gen = {}
+    for i, c in enumerate(cands):
+        if costs[i] < INF and not c.get("extra_outputs"):
+            gen[frozenset(c["members"])] = i
+    nodes = prim_graph["nodes"]
+    succ = {n["id"]: set() for n in nodes}
+    for n in nodes:
+        for r in n["inputs"]:
+            if "node" in r:
+                succ[r["node"]].add(n["id"])
+    group = {n["id"]: frozenset([n["id"]]) for n in nodes}   # primitive -> its kernel's members
+    topo = prim_graph_topo(prim_graph)
+    for v in sorted(succ, key=lambda x: -topo[x]):
+        g = group[v]
+        sinks = [u for u in g if not (succ[u] & g)]
+        if len(sinks) != 1 or sinks[0] != v or v in outputs:
+            continue
+        consumers = {frozenset(group[w]) for w in succ[v]}
+        if len(consumers) != 1:
+            continue
+        (cg,) = consumers
+        merged = g | cg
+        if merged in gen:
+            for u in merged:
+                group[u] = merged
+    kernels = set(group.values())
+    if any(g not in gen for g in kernels):
+        raise ValueError("greedy fusion left a kernel with no generable candidate")
+    return sorted(gen[g] for g in kernels)
+
+
+_TOPO_CACHE = {}
+
+
+def prim_graph_topo(prim_graph):
+    key = id(prim_graph)
+    if key not in _TOPO_CACHE:
+        import heapq
+        nodes = prim_graph["nodes"]
+        preds = {n["id"]: {r["node"] for r in n["inputs"] if "node" in r} for n in nodes}
+        succ = {v: [] for v in preds}
+        for v, ps in preds.items():
+            for u in ps:
+                succ[u].append(v)
+        indeg = {v: len(p) for v, p in preds.items()}
+        ready = [v for v, d in indeg.items() if not d]
+        heapq.heapify(ready)
+        pos = {}
+        while ready:
+            v = heapq.heappop(ready)
+            pos[v] = len(pos)
+            for w in succ[v]:
+                indeg[w] -= 1
+                if not indeg[w]:
+                    heapq.heappush(ready, w)
+        _TOPO_CACHE[key] = pos
+    return _TOPO_CACHE[key]

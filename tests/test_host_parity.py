@@ -355,3 +355,35 @@ def test_multi_output_blp_equals_oracle_search_c1(ctx):
         assert obj == want
         assert feasible_mo(mo, sel, sorted(G.outputs), cin, G.topo_index)
         kg.set_orchestration(sel)          # the library accepts it (Eq. 3 / Eq. 4')
+
+
+@pytest.mark.parametrize("name", ["c1", "c2", "misc", "cnn"])
+def test_greedy_fusion_ablation_is_feasible_and_never_beats_blp(ctx, name):
+    """Fission + greedy fusion (P:505-518 ablation; P:611-616 'fuse everything'): a
+    feasible partition (oracle Eq. 3/4 check) whose cost is never below the BLP optimum."""
+    from paper_2406_09465_b200.select import greedy_fusion
+    g = GRAPHS[name]()
+    kg = KorchGraph(ctx, g)
+    cands = kg.enumerate()
+    G, ref = _oracle_cands(g)
+    cin = [candidate_inputs(G, m) for m, _ in ref]
+    rng = np.random.default_rng(2)
+    for _ in range(3):
+        costs = [int(rng.integers(100, 5000)) if c["klass"] != "rejected" else (1 << 63) - 1 for c in cands]
+        sel = greedy_fusion(cands, costs, kg.prim, kg.outputs)
+        assert feasible(ref, sel, sorted(G.outputs), cin)
+        members = sorted(m for i in sel for m in cands[i]["members"])
+        assert members == list(range(kg.n_prims))          # a partition: no redundancy
+        obj, _ = solve_blp(cands, costs, kg.outputs)
+        assert obj <= sum(costs[i] for i in sel)
+
+
+def test_greedy_fusion_fuses_c1_into_one_kernel(ctx):
+    """C1's 15 primitives form one generable candidate; every producer's consumers end up
+    in one kernel, so greedy fusion selects exactly that whole-block kernel."""
+    from paper_2406_09465_b200.select import greedy_fusion
+    kg = KorchGraph(ctx, c1_softmax_layernorm())
+    cands = kg.enumerate()
+    costs = [1000 if c["klass"] != "rejected" else (1 << 63) - 1 for c in cands]
+    sel = greedy_fusion(cands, costs, kg.prim, kg.outputs)
+    assert len(sel) == 1 and len(cands[sel[0]]["members"]) == kg.n_prims
