@@ -1195,9 +1195,14 @@ static const KernelVariant& copy_variant() {
   return v;
 }
 
+// Above this size host<->device transfers use copy-engine memcpy nodes (DMA at full link
+// bandwidth) instead of copy kernels / kernel stores over mapped host memory.
+static const size_t kHostKernelCopyMax = 1u << 20;
+
 static bool launch_copy(korch_ctx* ctx, const void* src, void* dst, size_t bytes, CUstream stream, bool pdl) {
   CudaApi& cu = cuda();
   if (((unsigned long long)src | (unsigned long long)dst | bytes) & 15) return false;
+  if (bytes > kHostKernelCopyMax) return false;
   CUdeviceptr ds = 0, dd = 0;
   if (cu.cuPointerGetAttribute(&ds, CU_POINTER_ATTRIBUTE_DEVICE_POINTER, (CUdeviceptr)src) != CUDA_SUCCESS) return false;
   if (cu.cuPointerGetAttribute(&dd, CU_POINTER_ATTRIBUTE_DEVICE_POINTER, (CUdeviceptr)dst) != CUDA_SUCCESS) return false;
@@ -1259,7 +1264,10 @@ korch_status korch_execute_host(korch_graph* G, const void* const* host_inputs, 
         if (a.kind == BufRef::Output) read_in_plan[a.index] = true;
     for (size_t j = 0; j < g.outputs.size(); ++j) {
       CUdeviceptr d = 0;
+      // (small outputs only: a kernel's scattered stores over the host link run far below
+      // the copy engine's bandwidth once the output is more than a few hundred KB)
       if (!ce_only && !read_in_plan[j] && host_outputs[j] && ((unsigned long long)host_outputs[j] & 15) == 0 &&
+          (size_t)tensor_bytes(g, Ref{false, g.outputs[j]}) <= kHostKernelCopyMax &&
           cu.cuPointerGetAttribute(&d, CU_POINTER_ATTRIBUTE_DEVICE_POINTER, (CUdeviceptr)host_outputs[j]) ==
               CUDA_SUCCESS)
         direct_out[j] = (void*)d;

@@ -799,3 +799,62 @@ def test_gemm_shapes(ctx, m, k, n, batch):
     for x in c.cands:
         if x["klass"] != "rejected":
             c.check(c.completion([x["index"]]))
+
+
+def _dconv_graph(kind, dtype="bf16"):
+    """Convolutions the direct-conv template (KB7 stencil) targets, with the operand chains
+    and epilogues of the paper models: Candy's reflect-padded 9x9 layers (few input
+    channels / few filters), an EfficientViT-style strided stem with HardSwish, YOLOX's
+    Focus space-to-depth in front of its stem conv with SiLU, and a depthwise window on an
+    elementwise input."""
+    b = GraphBuilder(dtype)
+    if kind == "candy_out":          # reflect pad -> 9x9 conv 16 -> 3 (+bias)
+        x = b.input("x", [1, 16, 24, 32])
+        h = b.op("Pad", x, pads=[[0, 0], [0, 0], [4, 4], [4, 4]], mode="reflect")
+        y = b.op("Conv", h, b.input("w", [3, 16, 9, 9], std=0.03), b.input("bias", [3], std=0.1),
+                 stride=[1, 1], pads=[0, 0], groups=1)
+    elif kind == "candy_in":         # reflect pad -> 9x9 conv 3 -> 32 (+bias) -> relu
+        x = b.input("x", [1, 3, 20, 40])
+        h = b.op("Pad", x, pads=[[0, 0], [0, 0], [4, 4], [4, 4]], mode="reflect")
+        y = b.op("Relu", b.op("Conv", h, b.input("w", [32, 3, 9, 9], std=0.06), b.input("bias", [32], std=0.1),
+                              stride=[1, 1], pads=[0, 0], groups=1))
+    elif kind == "stem":             # 3x3 s2 conv 3 -> 16 (+bias) -> hardswish, zero padding
+        x = b.input("x", [2, 3, 34, 64])
+        y = b.op("HardSwish", b.op("Conv", x, b.input("w", [16, 3, 3, 3], std=0.2), b.input("bias", [16], std=0.1),
+                                   stride=[2, 2], pads=[1, 1], groups=1))
+    elif kind == "focus":            # space-to-depth (reshape/transpose) -> 3x3 conv 12 -> 16 -> SiLU
+        x = b.input("x", [1, 3, 32, 48])
+        f = b.op("Reshape", x, shape=[1, 3, 16, 2, 24, 2])
+        f = b.op("Transpose", f, perm=[0, 5, 3, 1, 2, 4])
+        f = b.op("Reshape", f, shape=[1, 12, 16, 24])
+        y = b.op("SiLU", b.op("Conv", f, b.input("w", [16, 12, 3, 3], std=0.1), b.input("bias", [16], std=0.1),
+                              stride=[1, 1], pads=[1, 1], groups=1))
+    else:                            # hardswish -> depthwise 3x3 (+bias) -> hardswish
+        x = b.input("x", [1, 40, 18, 32])
+        y = b.op("HardSwish", b.op("Conv", b.op("HardSwish", x), b.input("w", [40, 1, 3, 3], std=0.3),
+                                   b.input("bias", [40], std=0.1), stride=[1, 1], pads=[1, 1], groups=40))
+    b.output(y)
+    return b.build()
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("dtype", ["bf16", "f32"])
+@pytest.mark.parametrize("kind", ["candy_out", "candy_in", "stem", "focus", "depthwise"])
+def test_direct_conv_every_variant(ctx, kind, dtype):
+    """KB7 direct-convolution variants: for every candidate that carries them, each
+    direct-conv launch variant inside a feasible orchestration matches the oracle (staged
+    operand chains with reflect / zero padding and layout views, channel chunking, tails,
+    epilogues)."""
+    c = Case(ctx, _dconv_graph(kind, dtype))
+    ran = 0
+    for x in c.cands:
+        if x["klass"] == "rejected":
+            continue
+        names = c.kg.variant_names(x["index"])
+        for v, nm in enumerate(names):
+            if not nm.startswith("korch_dconv"):
+                continue
+            c.kg.set_variant(x["index"], v)
+            c.check(c.completion([x["index"]]))
+            ran += 1
+    assert ran >= 2
