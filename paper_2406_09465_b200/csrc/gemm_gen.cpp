@@ -383,6 +383,16 @@ static KernelPlan generate_matmul_gather(const Graph& g, const Candidate& c, int
   el << "          const size_t idx = " << vb.off << " + (size_t)kg * " << vb.coef[nbB] << " + (size_t)p * " << vb.coef[nbB + 1]
      << ";\n";
   gs.elem = el.str();
+  if (vb.coef[nbB + 1] == 1) {
+    // N-contiguous B (a weight whose row pitch is not 16-byte aligned, e.g. SegFormer's
+    // 150-class classifier, or a [C, HW] activation with HW = 196 / 676): a group of 8
+    // consecutive columns of one K row is one unaligned 16-byte read
+    std::ostringstream ve;
+    ve << "        const int p0 = tile_n + grp * 8;\n";
+    ve << "        const bool vok = kg < " << K << " && p0 + 7 < " << N << ";\n";
+    ve << "        const size_t vidx = " << vb.off << " + (size_t)kg * " << vb.coef[nbB] << " + (size_t)p0;\n";
+    gs.vec = ve.str();
+  }
   std::ostringstream t;
   t << "gemm-gatherB M=" << M << " N=" << N << " K=" << K;
   gs.tag = t.str();

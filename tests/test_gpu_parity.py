@@ -858,3 +858,40 @@ def test_direct_conv_every_variant(ctx, kind, dtype):
             c.check(c.completion([x["index"]]))
             ran += 1
     assert ran >= 2
+
+
+def _gather_b_graph(m, k, n, b_layout, dtype="bf16"):
+    """MatMuls whose B view has no 16-byte-aligned row pitch (gather-B tcgen05 GEMM):
+    'wn' = a [K, N] weight with odd N (SegFormer's 150-class classifier), 'chw' = the
+    [C, HW] activation of a pointwise conv with HW = 196 / 676 (EfficientViT / YOLOX)."""
+    b = GraphBuilder(dtype)
+    if b_layout == "wn":
+        x = b.input("x", [1, m, k])
+        y = b.op("Add", b.op("MatMul", x, b.input("w", [k, n], std=k ** -0.5)), b.input("bias", [n], std=0.1))
+    else:
+        x = b.input("x", [1, k, n])                       # [1, C, HW]
+        t = b.op("Reshape", x, shape=[k, n])
+        y = b.op("SiLU", b.op("Add", b.op("MatMul", b.input("w", [m, k], std=k ** -0.5), t),
+                                b.input("bias", [m, 1], std=0.1)))
+    b.output(y)
+    return b.build()
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("m,k,n,lay", [(300, 256, 150, "wn"), (128, 64, 19, "wn"), (64, 128, 196, "chw"),
+                                       (96, 64, 676, "chw")])
+def test_gather_b_gemm_every_variant(ctx, m, k, n, lay):
+    """Gather-B GEMM (B gathered into the MN-major SW128 layout by four producer warps;
+    8 consecutive columns per 16-byte unaligned read when B is N-contiguous): every
+    launch variant of every GEMM candidate, ragged M / N tails."""
+    c = Case(ctx, _gather_b_graph(m, k, n, lay))
+    gg = [x for x in c.cands if x["klass"] == "gemm"]
+    assert gg
+    ran = 0
+    for x in gg:
+        nv, _, _ = c.kg.variant_info(x["index"])
+        for v in range(nv):
+            c.kg.set_variant(x["index"], v)
+            c.check(c.completion([x["index"]]))
+            ran += 1
+    assert ran >= 2
