@@ -189,9 +189,7 @@ TUNING_DB = os.path.join(ROOT, "profiles", "tuning_db")
 
 def model_graph(name: str, batch: int = 1):
     from korch_workloads.models import MODELS
-    if batch != 1:
-        raise ValueError("whole models are built at batch 1")
-    return MODELS[name]()
+    return MODELS[name]() if batch == 1 else MODELS[name](batch=batch)
 
 
 def model_enum_opts(kg) -> dict:
@@ -338,6 +336,14 @@ def run_model(K, name, pk, steps=50, oracle_check=True, retune=False, db_dir=TUN
             "variant": kg.variant_info(i)[2], "name": kg.kernel_name(i)}
            for i in sorted(order, key=lambda i: -costs[i])[:5]]
     base_lat, base_clocks, _, _ = measure(base)
+    # fission + greedy fusion without the BLP (P:505-518 ablation, reading A35), same costs
+    greedy = S.greedy_fusion(cands, costs, kg.prim, kg.outputs)
+    try:
+        g_lat, _, _, _ = measure(greedy)
+        res["greedy_fusion"] = {"latency_ms": g_lat["p50"], "kernels": len(greedy),
+                                "objective_ns": sum(costs[i] for i in greedy)}
+    except Exception as e:  # reported, never silently replaced
+        res["greedy_fusion"] = {"error": f"{type(e).__name__}: {e}"[:300], "kernels": len(greedy)}
     res.update({"latency_ms": lat["p50"], "latency_ms_dist": lat, "clocks": clocks, "kernels": len(order),
                 "e2e_ms": statistics.median(e2e), "e2e_h2d_bytes": host_x.numel() * host_x.element_size(),
                 "e2e_d2h_bytes": sum(t.numel() * t.element_size() for t in host_out), "e2e_output_matches": e2e_match,
@@ -368,6 +374,90 @@ def run_model(K, name, pk, steps=50, oracle_check=True, retune=False, db_dir=TUN
     print("[models] " + json.dumps({name: {k: res[k] for k in ("latency_ms", "operator_aligned_ms", "kernels",
                                                              "blp_optimal", "wall_s")}}), file=sys.stderr, flush=True)
     del kg, outs, dev, ws
+    ctx.close()
+    torch.cuda.empty_cache()
+    return res
+
+
+SCALING_MODELS = ["efficientvit", "yolox", "candy"]   # BASELINE configs C3 (EfficientViT) and C5 (YOLOX / Candy)
+SCALING_GLOBAL_BATCH = 8
+
+
+def model_batch_throughput(K, name, pk, global_batch=SCALING_GLOBAL_BATCH, steps=20, flush=None, coll_dev=None,
+                           db_dir=TUNING_DB):
+    """BASELINE C3 / C5: a paper model at a global batch sharded over the
+    ranks.  Each rank runs the orchestration selected for its LOCAL batch (reading A26;
+    costs from the tuning database recorded at that batch, else profiled live with the
+    candidates shared round-robin across ranks and MIN-all-reduced, G1), with no
+    communication on the data path; the step time is the max over ranks (G4) and the
+    output shards are all-gathered afterwards (G3, outside the timed region)."""
+    import torch
+    import torch.distributed as dist
+    import paper_2406_09465_b200.select as S
+    from korch_workloads import make_inputs
+    from paper_2406_09465_b200 import tunedb
+    from paper_2406_09465_b200.dist import max_over_ranks, merge_costs, my_share, shard, world
+    rank, ws_, _ = world()
+    lo, hi = shard(global_batch, rank, ws_)
+    batch = hi - lo
+    graph = model_graph(name, batch)
+    ctx = K.Context(torch.cuda.current_device())
+    kg = K.KorchGraph(ctx, graph)
+    opts = model_enum_opts(kg)
+    cands = kg.enumerate(**opts)
+    t0 = time.perf_counter()
+    db_path = os.path.join(db_dir, f"{name}_b{batch}.json")
+    db = tunedb.load(db_path)
+    ok, why = tunedb.usable(db, graph, opts)
+    if ok:
+        costs, missing = tunedb.apply(kg, db)
+        if missing:
+            for i, c in zip(missing, kg.profile(missing)):
+                costs[i] = c
+        source = f"tuning database {os.path.relpath(db_path, ROOT)} ({len(missing)} profiled live)"
+    elif ws_ > 1 and global_batch % ws_ == 0:
+        kg.compile()
+        mine = my_share(len(cands), rank, ws_)
+        part = kg.profile(mine)
+        costs, variants = merge_costs(mine, part, [kg.variant_info(i)[1] for i in mine], len(cands), device=coll_dev)
+        for i, v in enumerate(variants):
+            if v >= 0:
+                kg.set_variant(i, v)
+        source = f"profiled live, sharded over {ws_} ranks ({why})"
+    else:
+        kg.compile()
+        costs = kg.profile()
+        source = f"profiled live ({why})"
+    obj, sel = kg.select(costs)
+    t_tune = time.perf_counter() - t0
+    ins = make_inputs(graph, seed=100 + rank)
+    dev = K.torch_inputs(graph, {k: v[1] for k, v in ins.items()})
+    stream = torch.cuda.current_stream()
+    if flush is None:
+        flush = torch.empty(512 << 20, dtype=torch.uint8, device="cuda")
+    kg.set_orchestration(sel)
+    outs, wsb = kg.torch_outputs(), kg.torch_workspace()
+    for _ in range(5):
+        kg.execute(dev, outs, wsb, stream)
+    if ws_ > 1:
+        dist.barrier()
+    ts = timed_steps(lambda: kg.execute(dev, outs, wsb, stream), stream, steps, flush)
+    ms = statistics.median(ts)
+    ms_max, = max_over_ranks([ms], device=coll_dev)
+    gather_ms = None
+    if ws_ > 1:
+        o = outs[0].contiguous() if coll_dev else outs[0].float().cpu()
+        bufs = [torch.empty_like(o) for _ in range(ws_)]
+        torch.cuda.synchronize()
+        t1 = time.perf_counter()
+        dist.all_gather(bufs, o)
+        torch.cuda.synchronize()
+        gather_ms = (time.perf_counter() - t1) * 1e3
+    res = {"global_batch": global_batch, "local_batch": batch, "n_gpus": ws_, "ms": ms_max, "ms_rank0": ms,
+           "throughput": {"value": global_batch / (ms_max * 1e-3), "unit": "images/s"},
+           "kernels": len(kg.plan()), "blp_objective_ns": obj, "blp_optimal": S.LAST_OPTIMAL, "tuning": source,
+           "tune_s": t_tune, "output_gather_ms_host_timed": gather_ms}
+    del kg, outs, dev, wsb
     ctx.close()
     torch.cuda.empty_cache()
     return res
@@ -548,6 +638,9 @@ def main():
     ap.add_argument("--models", default=",".join(DEFAULT_MODELS),
                     help="comma list of whole paper models to time at bs 1 ('' = none)")
     ap.add_argument("--retune", action="store_true", help="profile the models live instead of using the tuning database")
+    ap.add_argument("--scaling-models", default=",".join(SCALING_MODELS),
+                    help="models timed at --scaling-batch global batch, sharded over the ranks ('' = none)")
+    ap.add_argument("--scaling-batch", type=int, default=SCALING_GLOBAL_BATCH)
     ap.add_argument("--no-scaled", action="store_true", help="skip the C2 batch-64 measurement")
     ap.add_argument("--no-attention-pairs", action="store_true",
                     help="paper-faithful P:626 prune only (no fused two-GEMM attention candidates)")
@@ -781,6 +874,15 @@ def main():
                 lat_max, = max_over_ranks([lat], device=coll_dev)
                 models[m]["latency_ms_rank0"] = models[m].get("latency_ms")
                 models[m]["latency_ms"] = lat_max
+    model_scaling = None
+    if args.scaling_models:
+        model_scaling = {}
+        for m in [m for m in args.scaling_models.split(",") if m]:
+            try:
+                model_scaling[m] = model_batch_throughput(K, m, pk, global_batch=args.scaling_batch, flush=flush,
+                                                          coll_dev=coll_dev)
+            except Exception as e:  # reported, never silently replaced
+                model_scaling[m] = {"error": f"{type(e).__name__}: {e}"[:400]}
     scaled = None
     if not args.no_scaled and args.config == "c2":
         try:
@@ -827,6 +929,7 @@ def main():
             "roofline": roof,
             "bandwidth_variant": bw,
             "scaled_variant": scaled,
+            "model_batch_throughput": model_scaling,
             "cpu_baseline": cpu,
             "clocks": clk.summary(),
             "tuning": tuning,

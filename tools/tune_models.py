@@ -42,10 +42,12 @@ def tune(name, batch, out_dir):
     obj, sel = kg.select(costs)
     t_sel = time.perf_counter() - t1
     base = kg.operator_aligned()
+    greedy = S.greedy_fusion(kg.cands, costs, kg.prim, kg.outputs)     # P:505-518 ablation (A35)
     db = tunedb.record(kg, costs, graph, opts, extra={
         "model": name, "batch": batch, "n_candidates": len(cands), "n_generable": len(kg.generable()),
         "selection": sel, "objective_ns": obj, "blp_optimal": S.LAST_OPTIMAL, "solver": S.LAST_SOLVER,
         "operator_aligned": base, "operator_aligned_ns": sum(costs[i] for i in base),
+        "greedy_fusion": greedy, "greedy_fusion_ns": sum(costs[i] for i in greedy),
         "compile_failures": len(kg.compile_failures),
         "tuning_s": {"enumerate": t_enum, "compile": t_comp, "profile": t_prof, "select": t_sel}})
     path = os.path.join(out_dir, f"{name}_b{batch}.json")
