@@ -18,7 +18,7 @@ namespace korch {
   X(cuEventSynchronize) X(cuEventElapsedTime) X(cuStreamBeginCapture) X(cuStreamEndCapture)        \
   X(cuGraphInstantiateWithFlags) X(cuGraphLaunch) X(cuGraphExecDestroy) X(cuGraphDestroy)          \
   X(cuGetErrorString) X(cuTensorMapEncodeTiled) X(cuMemcpyHtoD) X(cuMemcpyDtoH)                 \
-  X(cuMemcpyHtoDAsync) X(cuMemcpyDtoHAsync) X(cuPointerGetAttribute) X(cuEventRecordWithFlags)
+  X(cuMemcpyHtoDAsync) X(cuMemcpyDtoHAsync) X(cuPointerGetAttribute) X(cuEventRecordWithFlags) X(cuStreamWaitEvent)
 
 struct CudaApi {
 #define KORCH_DECL(name) decltype(&::name) name = nullptr;

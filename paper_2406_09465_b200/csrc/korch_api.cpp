@@ -68,6 +68,8 @@ struct korch_ctx {
   int sm_count = 0;
   int l2_bytes = 0;
   CUstream pstream = nullptr;           // profiling / capture stream
+  std::vector<CUstream> aux;            // extra capture streams (concurrent plan branches, N4)
+  std::vector<CUevent> events;          // capture-time fork / join / step-completion events
   CUdeviceptr arena = 0;
   size_t arena_bytes = 0;
   CUdeviceptr flush = 0;
@@ -134,6 +136,7 @@ struct korch_graph {
   // accepted orchestration
   bool has_plan = false;
   std::vector<Step> steps;
+  std::vector<std::vector<int>> deps;  // steps each step must follow (RAW / WAR / WAW on buffers)
   size_t ws_bytes = 0;
   // captured executable
   std::vector<const void*> cap_ptrs, cap_ptrs_host;
@@ -540,6 +543,82 @@ static void launch_fill(korch_ctx* ctx, CUdeviceptr p, size_t elems, DType dt, u
   CU_CHECK(cuda().cuLaunchKernel(m->fn, grid, 1, 1, 256, 1, 1, 0, stream, args, nullptr));
 }
 
+// Launch the plan's steps into the capture running on ctx->pstream.  With KORCH_STREAMS
+// = k > 1 (default 4) independent steps go to different streams of the capture, so the
+// graph has parallel branches (overlap-aware execution): a step joins
+// the stream whose last step is one of its ancestors (the most recent one first, then a
+// fresh stream, else the oldest), waits on events of the dependencies that stream order
+// does not already imply, and keeps programmatic dependent launch behind the previous
+// kernel of its stream (never for a stream's first plan kernel: graph inputs may still be
+// in flight from host copies).  k = 1 is the sequential chain of reading A6.
+template <typename LaunchFn>
+static void capture_steps(korch_ctx* ctx, korch_graph* G, bool use_pdl, LaunchFn launch) {
+  CudaApi& cu = cuda();
+  static const int nstreams = [] {
+    const char* e = getenv("KORCH_STREAMS");
+    int v = e ? atoi(e) : 4;
+    return std::max(1, std::min(v, 8));
+  }();
+  const int ns = nstreams;
+  const size_t nsteps = G->steps.size();
+  while ((int)ctx->aux.size() < ns - 1) {
+    CUstream st;
+    CU_CHECK(cu.cuStreamCreate(&st, CU_STREAM_NON_BLOCKING));
+    ctx->aux.push_back(st);
+  }
+  while (ctx->events.size() < nsteps + 2 * (size_t)ns) {
+    CUevent ev;
+    CU_CHECK(cu.cuEventCreate(&ev, CU_EVENT_DISABLE_TIMING));
+    ctx->events.push_back(ev);
+  }
+  std::vector<CUstream> streams{ctx->pstream};
+  for (int i = 0; i + 1 < ns; ++i) streams.push_back(ctx->aux[i]);
+  if (ns > 1) {  // fork: every aux stream joins the capture after what pstream has so far
+    CUevent fork = ctx->events[nsteps];
+    CU_CHECK(cu.cuEventRecord(fork, ctx->pstream));
+    for (int i = 1; i < ns; ++i) CU_CHECK(cu.cuStreamWaitEvent(streams[i], fork, 0));
+  }
+  std::vector<int> last(ns, -1), where(nsteps, 0);
+  std::vector<std::vector<char>> anc(nsteps, std::vector<char>(nsteps, 0));
+  for (size_t t = 0; t < nsteps; ++t) {
+    const std::vector<int>& D = G->deps[t];
+    for (int d : D) {
+      anc[t][d] = 1;
+      for (size_t a = 0; a < nsteps; ++a) anc[t][a] = anc[t][a] || anc[d][a];
+    }
+    int sel = -1;
+    if (ns == 1) sel = 0;
+    else {
+      int best = -2;
+      for (int s = 0; s < ns; ++s) {  // the stream whose last step is the latest ancestor
+        int L = last[s];
+        if (L >= 0 && anc[t][L] && L > best) { best = L; sel = s; }
+      }
+      if (sel < 0)
+        for (int s = 0; s < ns && sel < 0; ++s)
+          if (last[s] < 0) sel = s;
+      if (sel < 0) {
+        int oldest = 1 << 30;
+        for (int s = 0; s < ns; ++s)
+          if (last[s] < oldest) { oldest = last[s]; sel = s; }
+      }
+    }
+    const int L = last[sel];
+    for (int d : D)
+      if (where[d] != sel || d > L)  // not implied by this stream's order
+        if (!(L >= 0 && (L == d || anc[L][d]))) CU_CHECK(cu.cuStreamWaitEvent(streams[sel], ctx->events[d], 0));
+    launch(G->steps[t], streams[sel], use_pdl && L >= 0);
+    if (ns > 1) CU_CHECK(cu.cuEventRecord(ctx->events[t], streams[sel]));
+    last[sel] = (int)t;
+    where[t] = sel;
+  }
+  for (int s = 1; s < ns; ++s) {  // join
+    CUevent j = ctx->events[nsteps + ns + s];
+    CU_CHECK(cu.cuEventRecord(j, streams[s]));
+    CU_CHECK(cu.cuStreamWaitEvent(ctx->pstream, j, 0));
+  }
+}
+
 // ------------------------------------------------------------------ API
 extern "C" {
 
@@ -596,6 +675,8 @@ korch_status korch_destroy(korch_ctx* c) {
     if (c->arena) cuda().cuMemFree(c->arena);
     if (c->flush) cuda().cuMemFree(c->flush);
     if (c->pstream) cuda().cuStreamDestroy(c->pstream);
+    for (CUstream st : c->aux) cuda().cuStreamDestroy(st);
+    for (CUevent ev : c->events) cuda().cuEventDestroy(ev);
     cuda().cuDevicePrimaryCtxRelease(c->dev);
   }
   delete c;
@@ -1088,6 +1169,35 @@ korch_status korch_set_orchestration(korch_graph* G, const int64_t* sel, int64_t
       for (auto& sc : scratch) release(sc.first, sc.second);
       steps.push_back(st);
     }
+    // step dependencies for concurrent replay (N4): step t follows step s < t when one
+    // writes a buffer range the other reads or writes (workspace ranges are reused by the
+    // liveness plan, so WAR / WAW matter as much as RAW)
+    {
+      struct Rg { int kind, idx; size_t lo, hi; };
+      auto rg = [&](const BufRef& b, size_t nb) {
+        if (b.kind == BufRef::Work) return Rg{2, 0, b.offset, b.offset + nb};
+        return Rg{b.kind == BufRef::Output ? 1 : 0, b.index, 0, nb};
+      };
+      auto ov = [](const Rg& a, const Rg& b) { return a.kind == b.kind && a.idx == b.idx && a.lo < b.hi && b.lo < a.hi; };
+      std::vector<std::vector<Rg>> rd(steps.size()), wr(steps.size());
+      for (size_t t = 0; t < steps.size(); ++t) {
+        const KernelPlan& kp = G->cs[steps[t].cand].plan;
+        for (size_t a = 0; a < steps[t].args.size(); ++a)
+          rd[t].push_back(rg(steps[t].args[a], (size_t)tensor_bytes(g, kp.ext[a])));
+        std::vector<int> os = outs_of(steps[t].cand);
+        for (size_t o = 0; o < steps[t].outs.size(); ++o)
+          wr[t].push_back(rg(steps[t].outs[o], (size_t)tensor_bytes(g, Ref{false, os[o]})));
+      }
+      G->deps.assign(steps.size(), {});
+      for (size_t t = 0; t < steps.size(); ++t)
+        for (size_t s2 = 0; s2 < t; ++s2) {
+          bool d = false;
+          for (auto& w : wr[s2]) for (auto& r : rd[t]) d = d || ov(w, r);
+          for (auto& r : rd[s2]) for (auto& w : wr[t]) d = d || ov(r, w);
+          for (auto& w : wr[s2]) for (auto& w2 : wr[t]) d = d || ov(w, w2);
+          if (d) G->deps[t].push_back((int)s2);
+        }
+    }
     G->steps = steps;
     G->ws_bytes = top;
     G->has_plan = true;
@@ -1150,13 +1260,13 @@ korch_status korch_execute(korch_graph* G, const void* const* inputs, void* cons
       std::lock_guard<std::mutex> cap(ctx->capture_mu);
       CU_CHECK(cu.cuStreamBeginCapture(ctx->pstream, CU_STREAM_CAPTURE_MODE_THREAD_LOCAL));
       try {
-        for (size_t k = 0; k < G->steps.size(); ++k) {
-          const Step& st = G->steps[k];
+        // every kernel after the first of its stream overlaps its prologue with its
+        // predecessor (PDL)
+        capture_steps(ctx, G, use_pdl, [&](const Step& st, CUstream sm, bool pdl) {
           std::vector<const void*> ins;
           for (auto& a : st.args) ins.push_back(resolve(a));
-          // every kernel after the first overlaps its prologue with its predecessor (PDL)
-          launch_variant(ctx, G->cs[st.cand].plan, st.variant, ins, resolve_outs(st), ctx->pstream, use_pdl && k > 0);
-        }
+          launch_variant(ctx, G->cs[st.cand].plan, st.variant, ins, resolve_outs(st), sm, pdl);
+        });
       } catch (...) {
         CUgraph tmp = nullptr;
         cu.cuStreamEndCapture(ctx->pstream, &tmp);
@@ -1299,16 +1409,15 @@ korch_status korch_execute_host(korch_graph* G, const void* const* host_inputs, 
               CU_CHECK(cu.cuMemcpyHtoDAsync((CUdeviceptr)dev_inputs[i], host_inputs[i], nb, ctx->pstream));
             any = true;
           }
-        for (size_t k = 0; k < G->steps.size(); ++k) {
-          const Step& st = G->steps[k];
+        // the first plan kernel of every stream is launched WITHOUT programmatic
+        // serialisation: plan kernels fetch graph inputs (weights, residual tiles, a staged
+        // LayerNorm input) before griddepcontrol.wait, and here the inputs are being written
+        // by the copy kernels just launched, so the plan may only start once they completed
+        capture_steps(ctx, G, use_pdl, [&](const Step& st, CUstream sm, bool pdl) {
           std::vector<const void*> ins;
           for (auto& a : st.args) ins.push_back(resolve(a));
-          // the first plan kernel is launched WITHOUT programmatic serialisation: plan
-          // kernels fetch graph inputs (weights, residual tiles, a staged LayerNorm input)
-          // before griddepcontrol.wait, and here the inputs are being written by the copy
-          // kernels just launched, so the plan may only start once they have completed
-          launch_variant(ctx, G->cs[st.cand].plan, st.variant, ins, resolve_outs(st), ctx->pstream, use_pdl && k > 0);
-        }
+          launch_variant(ctx, G->cs[st.cand].plan, st.variant, ins, resolve_outs(st), sm, pdl);
+        });
         for (size_t j = 0; j < g.outputs.size(); ++j)
           if (host_outputs[j] && !direct_out[j]) {
             const size_t nb = (size_t)tensor_bytes(g, Ref{false, g.outputs[j]});
