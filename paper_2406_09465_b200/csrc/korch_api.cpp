@@ -554,12 +554,8 @@ static void launch_fill(korch_ctx* ctx, CUdeviceptr p, size_t elems, DType dt, u
 template <typename LaunchFn>
 static void capture_steps(korch_ctx* ctx, korch_graph* G, bool use_pdl, LaunchFn launch) {
   CudaApi& cu = cuda();
-  static const int nstreams = [] {
-    const char* e = getenv("KORCH_STREAMS");
-    int v = e ? atoi(e) : 4;
-    return std::max(1, std::min(v, 8));
-  }();
-  const int ns = nstreams;
+  const char* env = getenv("KORCH_STREAMS");  // read per capture (tests compare settings)
+  const int ns = std::max(1, std::min(env ? atoi(env) : 4, 8));
   const size_t nsteps = G->steps.size();
   while ((int)ctx->aux.size() < ns - 1) {
     CUstream st;
