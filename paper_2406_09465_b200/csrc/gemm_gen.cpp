@@ -1635,6 +1635,138 @@ KernelPlan generate_attention(const Graph& g, const Candidate& c) {
   kp.variants.push_back(kv);
   kp.klass = KORCH_CLASS_GEMM;
   kp.reject.clear();
+
+  // Variant 2: the softmax of S spread over 16 warps (4 threads per row).  TMEM lane
+  // quarter q is readable by warps q, q+4, q+8, q+12; each loads a quarter of S's columns
+  // for its 32 rows into a per-quarter staging buffer (named barrier per quarter), then
+  // re-reads 8 rows x 4 lanes per row, so every thread owns N1/4 columns of one row and
+  // the row reductions are 2-step shuffles: 4x less serial work per thread than one row
+  // per thread.  Warps 16 / 17 issue TMA / MMA; the O epilogue stays on warps 0-3.
+  if (N1 <= 128) {
+    GemmEpilogue ep1s;
+    std::string e3;
+    if (make_gemm_epilogue(g, c, lin[0], (int)N1, pre, &ep1s, &e3, pnode, 4) && ep1s.ext.size() == ep1.ext.size() &&
+        std::equal(ep1s.ext.begin(), ep1s.ext.end(), ep1.ext.begin(),
+                   [](const Ref& a, const Ref& b) { return a.is_input == b.is_input && a.id == b.id; })) {
+      const int CQ = (int)N1 / 4, PIT = (int)N1 + 4;
+      const int offS = offP + P_BYTES, S_BYTES = 4 * 32 * PIT * 4;
+      const int offB2 = offS + S_BYTES;
+      const int smem2 = offB2 + 64 + 1024;
+      std::ostringstream q;
+      q << "extern \"C\" __global__ void __launch_bounds__(576, 1) KNAME(";
+      for (size_t i = 0; i < kp.ext.size(); ++i)
+        q << "const " << (g.dtype_of(kp.ext[i]) == DType::F32 ? "float" : "bf16_t") << "* __restrict__ p" << i << ", ";
+      q << (g.prims[c.output].dtype == DType::F32 ? "float" : "bf16_t") << "* __restrict__ out" << extra_out_params(g, c) << ", "
+        << "const __grid_constant__ TmaMap tmQ, const __grid_constant__ TmaMap tmK, const __grid_constant__ TmaMap tmV) {\n";
+      q << "  typedef int idx_t;\n";
+      q << "  extern __shared__ __align__(1024) unsigned char smem_raw[];\n";
+      q << "  unsigned char* smem = (unsigned char*)(((unsigned long long)smem_raw + 1023ull) & ~1023ull);\n";
+      q << "  unsigned long long* bars = (unsigned long long*)(smem + " << offB2 << ");\n";
+      q << "  unsigned long long *ldf = bars, *sfull = bars + 1, *pfull = bars + 2, *ofull = bars + 3, *ldv = bars + 4;\n";
+      q << "  unsigned* tslot = (unsigned*)(bars + 5);\n";
+      q << "  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;\n";
+      q << "  const int tile_m = blockIdx.x * 128;\n";
+      q << "  int bzl = blockIdx.z;\n";
+      for (int b = nb - 1; b >= 0; --b) q << "  const int bz" << b << " = bzl % " << SS[b] << "; bzl /= " << SS[b] << ";\n";
+      q << "  (void)bzl;\n";
+      q << "  if (threadIdx.x == 0) {\n    mbar_init(ldf, 1); mbar_init(sfull, 1); mbar_init(pfull, 16); mbar_init(ofull, 1);\n"
+        << "    mbar_init(ldv, 1);\n"
+        << "    mbar_fence_init();\n    tma_prefetch(&tmQ); tma_prefetch(&tmK); tma_prefetch(&tmV);\n  }\n";
+      q << "  if (warp == 17) tc_alloc(tslot, " << tcols << ");\n";
+      q << "  tc_fence_before();\n  __syncthreads();\n  tc_fence_after();\n";
+      q << "  const unsigned tmem = *tslot;\n";
+      q << "  pdl_trigger();\n  pdl_wait();\n";
+      q << "  if (warp == 16 && lane == 0) {\n";
+      q << "    mbar_expect_tx(ldf, " << Q_BYTES + K_BYTES << "u);\n";
+      q << "    mbar_expect_tx(ldv, " << V_BYTES << "u);\n";
+      for (int64_t kb = 0; kb < KB1; ++kb) {
+        q << "    " << load(dq.rank) << "(smem + " << kb * 16384 << ", &tmQ, ldf, " << coords(std::to_string(kb * 64), "tile_m", bq) << ");\n";
+        q << "    " << load(dk.rank) << "(smem + " << offK + kb * N1 * 128 << ", &tmK, ldf, " << coords(std::to_string(kb * 64), "0", bk) << ");\n";
+      }
+      if (v_n) {
+        for (int64_t cc = 0; cc < (N2 + 63) / 64; ++cc)
+          q << "    " << load(dv.rank) << "(smem + " << offV + cc * N1 * 128 << ", &tmV, ldv, " << coords(std::to_string(cc * 64), "0", bv) << ");\n";
+      } else {
+        for (int64_t cc = 0; cc < N1 / 64; ++cc)
+          q << "    " << load(dv.rank) << "(smem + " << offV + cc * N2 * 128 << ", &tmV, ldv, " << coords(std::to_string(cc * 64), "0", bv) << ");\n";
+      }
+      q << "  } else if (warp == 17 && lane == 0) {\n";
+      q << "    mbar_wait(ldf, 0);\n    tc_fence_after();\n";
+      q << "    const unsigned sq = smem_u32(smem), sk = sq + " << offK << ", sv = sq + " << offV << ", sp = sq + " << offP << ";\n";
+      q << "    #pragma unroll\n    for (int kb = 0; kb < " << KB1 << "; ++kb)\n";
+      q << "      #pragma unroll\n      for (int k = 0; k < 4; ++k)\n";
+      q << "        tc_mma(tmem, umma_desc(sq + kb * 16384 + k * 32, 16, 1024), umma_desc(sk + kb * " << N1 * 128
+        << " + k * 32, 16, 1024), " << id1 << "u, (kb | k) != 0);\n";
+      q << "    tc_commit(sfull);\n";
+      q << "    mbar_wait(pfull, 0);\n    mbar_wait(ldv, 0);\n    tc_fence_after();\n";
+      q << "    #pragma unroll\n    for (int k0 = 0; k0 < " << N1 << "; k0 += 16) {\n";
+      q << "      const unsigned long long ad = umma_desc(sp + (k0 >> 6) * 16384 + (k0 & 63) * 2, 16, 1024);\n";
+      if (v_n)
+        q << "      const unsigned long long bd = umma_desc(sv + k0 * 128, " << N1 * 128 << ", 1024);\n";
+      else
+        q << "      const unsigned long long bd = umma_desc(sv + (k0 >> 6) * " << N2 * 128 << " + (k0 & 63) * 2, 16, 1024);\n";
+      q << "      tc_mma(tmem + " << N1 << ", ad, bd, " << id2 << "u, k0 != 0);\n    }\n";
+      q << "    tc_commit(ofull);\n  }\n";
+      q << "  __syncwarp();\n";
+      q << "  if (warp < 16) {\n";
+      q << "    const int qq = warp & 3, cq = warp >> 2;\n";
+      q << "    float* stq = reinterpret_cast<float*>(smem + " << offS << ") + qq * " << 32 * PIT << ";\n";
+      q << "    mbar_wait(sfull, 0);\n    __syncwarp();\n    tc_fence_after();\n";
+      q << "    {\n      float accq[" << CQ << "];\n";
+      if (CQ == 16) q << "      tc_ld16(tmem + ((unsigned)(qq * 32) << 16) + (unsigned)(cq * 16), accq);\n";
+      else
+        q << "      #pragma unroll\n      for (int u = 0; u < " << CQ / 32 << "; ++u)\n        tc_ld32(tmem + ((unsigned)(qq * 32) << 16) + (unsigned)(cq * "
+          << CQ << " + u * 32), accq + u * 32);\n";
+      q << "      #pragma unroll\n      for (int u = 0; u < " << CQ / 4 << "; ++u)\n"
+        << "        *reinterpret_cast<float4*>(stq + lane * " << PIT << " + cq * " << CQ << " + 4 * u) = make_float4(accq[4 * u], "
+           "accq[4 * u + 1], accq[4 * u + 2], accq[4 * u + 3]);\n    }\n";
+      q << "    asm volatile(\"bar.sync %0, 128;\" :: \"r\"(1 + qq) : \"memory\");\n";
+      q << "    {\n      const int rq = cq * 8 + (lane >> 2), tid = lane & 3;\n";
+      q << "      const int gm = tile_m + qq * 32 + rq;\n      const int nb = 0;\n      const unsigned gmask = 0xffffffffu;\n"
+        << "      (void)gmask;\n";
+      q << "      float acc[" << N1 / 4 << "];\n";
+      q << "      #pragma unroll\n      for (int k = 0; k < " << N1 / 32 << "; ++k) {\n";
+      q << "        const float4 a0 = *reinterpret_cast<const float4*>(stq + rq * " << PIT << " + (tid + k * 4) * 8);\n";
+      q << "        const float4 a1 = *reinterpret_cast<const float4*>(stq + rq * " << PIT << " + (tid + k * 4) * 8 + 4);\n";
+      q << "        acc[k * 8] = a0.x; acc[k * 8 + 1] = a0.y; acc[k * 8 + 2] = a0.z; acc[k * 8 + 3] = a0.w;\n";
+      q << "        acc[k * 8 + 4] = a1.x; acc[k * 8 + 5] = a1.y; acc[k * 8 + 6] = a1.z; acc[k * 8 + 7] = a1.w;\n      }\n";
+      q << ep1s.body;
+      q << "      const unsigned sp = smem_u32(smem + " << offP << ");\n";
+      q << "      const int r = qq * 32 + rq;\n";
+      q << "      #pragma unroll\n      for (int k = 0; k < " << N1 / 32 << "; ++k) {\n";
+      q << "        const int col = (tid + k * 4) * 8;\n";
+      q << "        uint4 pk = make_uint4(pack2(" << ep1s.store << "[k * 8], " << ep1s.store << "[k * 8 + 1]), pack2(" << ep1s.store
+        << "[k * 8 + 2], " << ep1s.store << "[k * 8 + 3]), pack2(" << ep1s.store << "[k * 8 + 4], " << ep1s.store
+        << "[k * 8 + 5]), pack2(" << ep1s.store << "[k * 8 + 6], " << ep1s.store << "[k * 8 + 7]));\n";
+      q << "        st_shared_v4(sp + (col >> 6) * 16384 + r * 128 + ((((col & 63) >> 3) ^ (r & 7)) << 4), pk);\n      }\n";
+      q << "    }\n";
+      q << "    fence_async_smem();\n    tc_fence_before();\n    __syncwarp();\n    if (lane == 0) mbar_arrive(pfull);\n";
+      q << "    if (warp < 4) {\n";
+      q << "      mbar_wait(ofull, 0);\n      __syncwarp();\n      tc_fence_after();\n";
+      q << "      const int tile_n = 0;\n      const unsigned tmem_o = tmem + " << N1 << ";\n";
+      q << "    " << emit_tmem_epilogue(ep2, (int)((N2 + 31) / 32 * 32), 32, TE2, M, N2, "tmem_o");
+      q << "    }\n  }\n";
+      q << "  tc_fence_before();\n  __syncthreads();\n";
+      q << "  if (warp == 17) tc_dealloc(tmem, " << tcols << ");\n}\n";
+      KernelVariant k2;
+      std::string s2 = q.str();
+      std::snprintf(nm, sizeof nm, "korch_attn_%016llx", (unsigned long long)fnv1a(std::string(kSm100GemmTemplate) + "\n" + s2));
+      k2.name = nm;
+      s2.replace(s2.find("KNAME"), 5, k2.name);
+      k2.source = s2;
+      k2.tcgen05 = true;
+      k2.block = 576;
+      k2.grid = (M + 127) / 128;
+      k2.grid_y = 1;
+      k2.grid_z = batch;
+      k2.smem = smem2;
+      k2.tma = {dq, dk, dv};
+      k2.tag = t.str() + " softmax=4/row";
+      if (smem2 <= 227 * 1024) kp.variants.push_back(k2);
+    } else if (getenv("KORCH_GEN_TRACE")) {
+      std::fprintf(stderr, "[attention split softmax] rejected: %s\n", e3.c_str());
+    }
+  }
   return kp;
 }
 
