@@ -441,7 +441,10 @@ def test_fused_attention_candidates(ctx, kw):
     if kw.get("seq", 128) % 64 == 0:
         assert att
     for i in att:
-        c.check(c.completion([i]))
+        nv, _, _ = c.kg.variant_info(i)   # one row per thread, and the 4-threads-per-row softmax
+        for v in range(nv):
+            c.kg.set_variant(i, v)
+            c.check(c.completion([i]))
     costs = c.kg.profile()
     obj, sel = c.kg.select(costs)
     c.check(sel)
