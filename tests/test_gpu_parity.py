@@ -898,3 +898,33 @@ def test_gather_b_gemm_every_variant(ctx, m, k, n, lay):
             c.check(c.completion([x["index"]]))
             ran += 1
     assert ran >= 2
+
+
+def _skinny_mm_graph(cin, cout, hw, dtype="bf16"):
+    """EfficientViT-style pointwise conv as MatMul over [C, HW] with few input channels
+    (+bias, HardSwish, back to NCHW)."""
+    b = GraphBuilder(dtype)
+    x = b.input("x", [1, cin, hw, hw])
+    t = b.op("Reshape", b.op("HardSwish", x), shape=[cin, hw * hw])
+    t = b.op("Add", b.op("MatMul", b.input("w", [cout, cin], std=cin ** -0.5), t), b.input("bias", [cout, 1], std=0.1))
+    b.output(b.op("HardSwish", b.op("Reshape", t, shape=[1, cout, hw, hw])))
+    return b.build()
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("cin,cout,hw", [(16, 64, 64), (32, 24, 40), (8, 200, 48)])
+@pytest.mark.parametrize("dtype", ["bf16", "f32"])
+def test_skinny_k_matmul_every_variant(ctx, cin, cout, hw, dtype):
+    """Skinny-K MatMul SIMT variants (K <= 64): every variant of every candidate carrying
+    them, including an elementwise chain on the staged B operand and ragged row groups."""
+    c = Case(ctx, _skinny_mm_graph(cin, cout, hw, dtype))
+    ran = 0
+    for x in c.cands:
+        if x["klass"] == "rejected":
+            continue
+        for v, nm in enumerate(c.kg.variant_names(x["index"])):
+            if nm.startswith("korch_skmm"):
+                c.kg.set_variant(x["index"], v)
+                c.check(c.completion([x["index"]]))
+                ran += 1
+    assert ran >= 2
