@@ -344,6 +344,36 @@ def run_model(K, name, pk, steps=50, oracle_check=True, retune=False, db_dir=TUN
                                 "objective_ns": sum(costs[i] for i in greedy)}
     except Exception as e:  # reported, never silently replaced
         res["greedy_fusion"] = {"error": f"{type(e).__name__}: {e}"[:300], "kernels": len(greedy)}
+    # N1 (reading A32): the same model with multi-output candidates, when a tuning database
+    # recorded with them exists (profiles/tuning_db/<model>_b1_mo2.json)
+    mo_db = tunedb.load(os.path.join(db_dir, f"{name}_b1_mo2.json"))
+    if mo_db is not None:
+        try:
+            mopts = dict(opts, max_outputs=2)
+            kg2 = K.KorchGraph(ctx, graph)
+            c2 = kg2.enumerate(**mopts)
+            ok2, why2 = tunedb.usable(mo_db, graph, mopts)
+            if ok2:
+                costs2, missing2 = tunedb.apply(kg2, mo_db)
+                for i, c in zip(missing2, kg2.profile(missing2) if missing2 else []):
+                    costs2[i] = c
+                obj2, sel2 = kg2.select(costs2)
+                kg2.set_orchestration(sel2)
+                o2, w2 = kg2.torch_outputs(), kg2.torch_workspace()
+                for _ in range(5):
+                    kg2.execute(dev, o2, w2, stream)
+                t2 = timed_steps(lambda: kg2.execute(dev, o2, w2, stream), stream, steps, flush)
+                same = all(torch.allclose(a.float(), b.float(), rtol=5e-2, atol=5e-2) for a, b in zip(o2, outs))
+                res["multi_output"] = {"latency_ms": statistics.median(t2), "kernels": len(kg2.plan()),
+                                       "objective_ns": obj2, "n_candidates": len(c2),
+                                       "kernels_with_secondary_outputs": sum(1 for i in sel2 if c2[i]["extra_outputs"]),
+                                       "blp_optimal": S.LAST_OPTIMAL, "profiled_live": len(missing2),
+                                       "outputs_close_to_single_output_plan": same}
+            else:
+                res["multi_output"] = {"skipped": why2}
+            del kg2
+        except Exception as e:  # reported, never silently replaced
+            res["multi_output"] = {"error": f"{type(e).__name__}: {e}"[:300]}
     res.update({"latency_ms": lat["p50"], "latency_ms_dist": lat, "clocks": clocks, "kernels": len(order),
                 "e2e_ms": statistics.median(e2e), "e2e_h2d_bytes": host_x.numel() * host_x.element_size(),
                 "e2e_d2h_bytes": sum(t.numel() * t.element_size() for t in host_out), "e2e_output_matches": e2e_match,

@@ -23,13 +23,15 @@ from paper_2406_09465_b200 import tunedb  # noqa: E402
 from bench import model_enum_opts, model_graph  # noqa: E402
 
 
-def tune(name, batch, out_dir):
+def tune(name, batch, out_dir, max_outputs=1):
     import torch
     t0 = time.perf_counter()
     graph = model_graph(name, batch)
     ctx = K.Context(torch.cuda.current_device())
     kg = K.KorchGraph(ctx, graph)
     opts = model_enum_opts(kg)
+    if max_outputs > 1:
+        opts["max_outputs"] = max_outputs     # N1 multi-output candidates (reading A32)
     cands = kg.enumerate(**opts)
     t_enum = time.perf_counter() - t0
     t1 = time.perf_counter()
@@ -50,7 +52,7 @@ def tune(name, batch, out_dir):
         "greedy_fusion": greedy, "greedy_fusion_ns": sum(costs[i] for i in greedy),
         "compile_failures": len(kg.compile_failures),
         "tuning_s": {"enumerate": t_enum, "compile": t_comp, "profile": t_prof, "select": t_sel}})
-    path = os.path.join(out_dir, f"{name}_b{batch}.json")
+    path = os.path.join(out_dir, f"{name}_b{batch}" + (f"_mo{max_outputs}" if max_outputs > 1 else "") + ".json")
     tunedb.save(path, db)
     print(f"[tune] {name} b{batch}: {len(cands)} candidates, compile {t_comp:.0f}s, profile {t_prof:.0f}s, "
           f"select {t_sel:.2f}s ({S.LAST_SOLVER}, optimal={S.LAST_OPTIMAL}), objective {obj} ns "
@@ -64,10 +66,11 @@ def main():
     ap.add_argument("models", nargs="+")
     ap.add_argument("--out", default=os.path.join(ROOT, "profiles", "tuning_db"))
     ap.add_argument("--batch", default="1", help="comma list of local batch sizes")
+    ap.add_argument("--max-outputs", type=int, default=1, help="> 1: also multi-output candidates (N1)")
     a = ap.parse_args()
     for b in [int(x) for x in a.batch.split(",")]:
         for m in a.models:
-            tune(m, b, a.out)
+            tune(m, b, a.out, a.max_outputs)
 
 
 if __name__ == "__main__":
