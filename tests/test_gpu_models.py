@@ -163,3 +163,18 @@ def test_paper_size_model_plan_matches_oracle(ctx, name):
         l2 = np.linalg.norm(got - r) / np.linalg.norm(r)
         mx = np.max(np.abs(got - r)) / np.max(np.abs(r))
         assert l2 <= 2e-2 and mx <= 5e-2, f"{name}: rel L2 {l2:.3e}, max-norm {mx:.3e}"
+
+
+@pytest.mark.gpu
+@pytest.mark.timeout(1800)
+@pytest.mark.parametrize("name", ["candy", "efficientvit", "yolox"])
+def test_batched_models_small(ctx, name):
+    """The batched model graphs of the C3 / C5 batch sweep (batch 2; batched pointwise
+    convolutions as token-major MatMuls) through the library, operator-aligned and
+    BLP-selected orchestrations against the oracle."""
+    from korch_workloads.models import efficientvit, yolox_nano
+    g = {"candy": lambda: candy(size=32, blocks=1, batch=2),
+         "efficientvit": lambda: efficientvit(size=64, depths=(1, 1, 1, 1, 1), batch=2),
+         "yolox": lambda: yolox_nano(size=64, batch=2)}[name]()
+    n, k_sel, k_base = _run_and_check(ctx, g)
+    assert n > 500
