@@ -225,11 +225,31 @@ def dist_summary(ts):
     return {"mean": statistics.mean(ts), "p10": pct(0.1), "p50": statistics.median(ts), "p90": pct(0.9)}
 
 
+# FP32 FMA peak of the SIMT kernels (direct convolution, skinny-K MatMul, SIMT
+# contractions): 148 SMs x 128 FP32 lanes x 2 flop x 1.965 GHz (B200_PROFILING.md unit
+# counts and the max SM clock)
+FP32_SIMT_TFLOPS = 148 * 128 * 2 * 1.965e9 / 1e12
+
+
 def roofline_of(kg, cands, i, cold_ns, pk):
-    """Roofline of candidate i from its algorithmic bytes / flops and a cold-L2 time."""
+    """Roofline of candidate i from its algorithmic bytes / flops and a cold-L2 time:
+    tcgen05 kernels against the bf16 tensor peak or HBM, SIMT kernels with flops
+    (direct conv, skinny-K MatMul) against the FP32 FMA peak ("alu") or HBM."""
     c = cands[i]
+    name = kg.kernel_name(i)
+    simt = not (name.startswith("korch_gemm") or name.startswith("korch_pgemm") or name.startswith("korch_conv")
+                or name.startswith("korch_gg") or name.startswith("korch_attn"))
+    if simt and c["flops"] > 0 and c["flops"] / (FP32_SIMT_TFLOPS * 1e12) > c["bytes"] / (pk["hbm_gbs"] * 1e9):
+        ach = c["flops"] / (cold_ns * 1e-9) / 1e12
+        r = {"bound": "alu", "achieved": ach, "peak": FP32_SIMT_TFLOPS, "unit": "TFLOP/s",
+             "peak_source": "148 SM x 128 FP32 lanes x 2 x 1.965 GHz"}
+        r["frac"] = r["achieved"] / r["peak"]
+        r.update({"traffic": load_ncu_traffic(name), "candidate": i, "class": c["klass"], "members": len(c["members"]),
+                  "algorithmic_bytes": c["bytes"], "flops": c["flops"], "ns_cold_l2": cold_ns, "name": name,
+                  "variant": kg.variant_info(i)[2]})
+        return r
     ridge = pk["bf16_tflops"] * 1e12 / (pk["hbm_gbs"] * 1e9)
-    ai = c["flops"] / max(1, c["bytes"]) if c["klass"] == "gemm" else 0.0
+    ai = c["flops"] / max(1, c["bytes"]) if c["klass"] == "gemm" and not simt else 0.0
     if ai > ridge:
         ach = c["flops"] / (cold_ns * 1e-9) / 1e12
         r = {"bound": "tensor", "achieved": ach, "peak": pk["bf16_tflops"], "unit": "TFLOP/s"}
@@ -237,7 +257,6 @@ def roofline_of(kg, cands, i, cold_ns, pk):
         ach = c["bytes"] / (cold_ns * 1e-9) / 1e9
         r = {"bound": "hbm", "achieved": ach, "peak": pk["hbm_gbs"], "unit": "GB/s"}
     r["frac"] = r["achieved"] / r["peak"]
-    name = kg.kernel_name(i)
     r.update({"traffic": load_ncu_traffic(name), "candidate": i, "class": c["klass"], "members": len(c["members"]),
               "algorithmic_bytes": c["bytes"], "flops": c["flops"], "ns_cold_l2": cold_ns, "name": name,
               "variant": kg.variant_info(i)[2]})
