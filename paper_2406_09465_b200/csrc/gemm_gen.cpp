@@ -498,11 +498,18 @@ static KernelPlan generate_gather_gemm(const Graph& g, const Candidate& c, int m
     k << "    for (int kb = kb0; kb < kb1; ++kb) {\n";
     k << "      mbar_wait(empty + s, ph ^ 1u);\n";
     k << "      const unsigned sb = smem_u32(smem + s * " << STAGE << " + " << A_BYTES << ");\n";
-    k << "      for (int u = threadIdx.x; u < " << 64 * (BN / 8) << "; u += 128) {\n";
+    // two phases: every group's global loads are issued before any shared-memory store
+    // (the stores are asm volatile with a memory clobber, which would otherwise serialise
+    // one L2 round trip per group)
+    const int ITERS = (64 * (BN / 8) + 127) / 128;
+    k << "      uint4 pks[" << ITERS << "];\n";
+    k << "      #pragma unroll\n      for (int itg = 0; itg < " << ITERS << "; ++itg) {\n";
+    k << "        const int u = threadIdx.x + itg * 128;\n";
     k << "        const int kk = u / " << BN / 8 << ", grp = u % " << BN / 8 << ";\n";
     k << "        const int kg = kb * 64 + kk;\n";
     k << gs.prologue;
-    k << "        uint4 pk;\n";
+    k << "        uint4 pk = make_uint4(0u, 0u, 0u, 0u);\n";
+    k << "        if (u < " << 64 * (BN / 8) << ") {\n";
     if (!gs.vec.empty()) {
       k << gs.vec;
       k << "        if (vok) {\n          pk = ld_bf16x8_unaligned(xin + vidx);\n        } else {\n";
@@ -518,8 +525,12 @@ static KernelPlan generate_gather_gemm(const Graph& g, const Candidate& c, int m
     k << "        pk.x = v[0] | ((unsigned)v[1] << 16); pk.y = v[2] | ((unsigned)v[3] << 16);\n";
     k << "        pk.z = v[4] | ((unsigned)v[5] << 16); pk.w = v[6] | ((unsigned)v[7] << 16);\n";
     k << "        }\n";
+    k << "        }\n        pks[itg] = pk;\n      }\n";
     // MN-major SW128 canonical: 64-pixel atoms 8 KB apart, K rows 128 B, 16B chunk ^ (row % 8)
-    k << "        st_shared_v4(sb + (grp >> 3) * 8192 + kk * 128 + (((grp & 7) ^ (kk & 7)) << 4), pk);\n";
+    k << "      #pragma unroll\n      for (int itg = 0; itg < " << ITERS << "; ++itg) {\n";
+    k << "        const int u = threadIdx.x + itg * 128;\n";
+    k << "        const int kk = u / " << BN / 8 << ", grp = u % " << BN / 8 << ";\n";
+    k << "        if (u < " << 64 * (BN / 8) << ") st_shared_v4(sb + (grp >> 3) * 8192 + kk * 128 + (((grp & 7) ^ (kk & 7)) << 4), pks[itg]);\n";
     k << "      }\n";
     k << "      fence_async_smem();\n      __syncwarp();\n";
     k << "      if (lane == 0) mbar_arrive(full + s);\n";
