@@ -928,3 +928,36 @@ def test_skinny_k_matmul_every_variant(ctx, cin, cout, hw, dtype):
                 c.check(c.completion([x["index"]]))
                 ran += 1
     assert ran >= 2
+
+
+def _ktv_graph(heads2=4, d=16, n=2048, dtype="bf16"):
+    """EfficientViT's LiteMLA K^T V: relu(K)^T [d, n] x pad_ones(V) [n, d+1] per
+    head over n tokens, K and V sliced out of a token-minor [2h, 3d, n] tensor."""
+    b = GraphBuilder(dtype)
+    x = b.input("x", [1, heads2, 3 * d, n])
+    ms = b.op("Transpose", x, perm=[0, 1, 3, 2])                        # [1, 2h, n, 3d]
+    k = b.op("Relu", b.op("Slice", ms, axis=3, start=d, end=2 * d))
+    v = b.op("Slice", ms, axis=3, start=2 * d, end=3 * d)
+    v = b.op("Pad", v, pads=[[0, 0], [0, 0], [0, 0], [0, 1]], mode="constant", value=1.0)
+    kv = b.op("MatMul", b.op("Transpose", k, perm=[0, 1, 3, 2]), v)     # [1, 2h, d, d+1]
+    b.output(b.op("MulC", kv, c=0.5))
+    return b.build()
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("n", [2048, 5000])
+@pytest.mark.parametrize("dtype", ["bf16", "f32"])
+def test_split_k_contraction_every_variant(ctx, n, dtype):
+    """KB8 cluster split-K contraction: every variant of every candidate carrying it
+    (operand chains staged per token tile, ragged K slices, DSMEM combine)."""
+    c = Case(ctx, _ktv_graph(n=n, dtype=dtype))
+    ran = 0
+    for x in c.cands:
+        if x["klass"] == "rejected":
+            continue
+        for v, nm in enumerate(c.kg.variant_names(x["index"])):
+            if nm.startswith("korch_kb8"):
+                c.kg.set_variant(x["index"], v)
+                c.check(c.completion([x["index"]]))
+                ran += 1
+    assert ran >= 1
