@@ -376,7 +376,7 @@ def run_model(K, name, pk, steps=50, oracle_check=True, retune=False, db_dir=TUN
                 costs2, missing2 = tunedb.apply(kg2, mo_db)
                 for i, c in zip(missing2, kg2.profile(missing2) if missing2 else []):
                     costs2[i] = c
-                obj2, sel2 = kg2.select(costs2)
+                obj2, sel2 = kg2.select(costs2, time_limit=60.0)
                 kg2.set_orchestration(sel2)
                 o2, w2 = kg2.torch_outputs(), kg2.torch_workspace()
                 for _ in range(5):
