@@ -283,7 +283,9 @@ static bool nvrtc_compile(const std::string& src, const std::string& name, std::
 }
 
 static void write_atomic(const std::string& path, const std::string& data) {
-  std::string tmp = path + ".tmp" + std::to_string((uintptr_t)&data) + std::to_string(std::hash<std::thread::id>()(std::this_thread::get_id()));
+  // unique per process and thread: several ranks may fill one cache directory at once
+  std::string tmp = path + ".tmp" + std::to_string((long)getpid()) + "_" +
+                    std::to_string(std::hash<std::thread::id>()(std::this_thread::get_id()));
   {
     std::ofstream f(tmp, std::ios::binary);
     f.write(data.data(), (std::streamsize)data.size());
