@@ -467,19 +467,30 @@ def model_batch_throughput(K, name, pk, global_batch=SCALING_GLOBAL_BATCH, steps
             for i, c in zip(missing, kg.profile(missing)):
                 costs[i] = c
         source = f"tuning database {os.path.relpath(db_path, ROOT)} ({len(missing)} profiled live)"
-    elif ws_ > 1 and global_batch % ws_ == 0:
-        kg.compile()
-        mine = my_share(len(cands), rank, ws_)
-        part = kg.profile(mine)
-        costs, variants = merge_costs(mine, part, [kg.variant_info(i)[1] for i in mine], len(cands), device=coll_dev)
-        for i, v in enumerate(variants):
-            if v >= 0:
-                kg.set_variant(i, v)
-        source = f"profiled live, sharded over {ws_} ranks ({why})"
     else:
-        kg.compile()
-        costs = kg.profile()
-        source = f"profiled live ({why})"
+        # No database at this local batch: a BOUNDED live search keeps the benchmark within
+        # minutes -- the operator-aligned kernels plus every candidate of <= 2 primitives
+        # (the full search is tools/tune_models.py --batch B, minutes to tens of minutes per
+        # model); the remaining candidates are left out (cost = INF), so the selection is
+        # optimal over this subset only and is reported as such.
+        base = set(kg.operator_aligned())
+        pool = [i for i in kg.generable() if i in base or len(cands[i]["members"]) <= 2]
+        kg.compile(pool)
+        costs = [K.INF] * len(cands)
+        if ws_ > 1 and global_batch % ws_ == 0:
+            mine = [pool[j] for j in my_share(len(pool), rank, ws_)]
+            part = kg.profile(mine)
+            merged, variants = merge_costs(mine, part, [kg.variant_info(i)[1] for i in mine], len(cands),
+                                           device=coll_dev)
+            for i in pool:
+                costs[i] = merged[i]
+                if variants[i] >= 0:
+                    kg.set_variant(i, variants[i])
+            source = f"bounded live search, sharded over {ws_} ranks ({why}): {len(pool)} candidates"
+        else:
+            for i, c in zip(pool, kg.profile(pool)):
+                costs[i] = c
+            source = f"bounded live search ({why}): {len(pool)} of {len(cands)} candidates"
     obj, sel = kg.select(costs)
     t_tune = time.perf_counter() - t0
     ins = make_inputs(graph, seed=100 + rank)

@@ -14,7 +14,7 @@
 namespace korch {
 
 struct TmaDesc {            // a 2-5D TMA tensor map the host encodes per launch
-  int tensor = -1;          // index into KernelPlan::ext (or -2 = output)
+  int tensor = -1;          // index into KernelPlan::ext (or -2 = output, -3 = the kernel's scratch)
   int rank = 0;
   int64_t dims[5] = {0};    // elements, innermost first
   int64_t strides[5] = {0}; // bytes, for dims 1..rank-1 (innermost stride is 1 element)

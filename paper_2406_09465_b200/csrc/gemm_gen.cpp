@@ -271,6 +271,55 @@ static std::string emit_dsmem_splitk(const GemmEpilogue& ep, int BN, int CW, int
   return k.str();
 }
 
+// The same reduction without cluster barriers on the critical path: the receive buffer
+// `recv` ([KS][RO][BN + 4] fp32) is a region of its own (not the operand ring), and
+// `rbar` (count 1, armed with the (KS - 1) * RO * BN * 4 remote bytes and published to the
+// cluster by a barrier before the programmatic-dependency wait) completes when every
+// peer's partial rows have landed: peers push with st.async ... mbarrier::complete_tx
+// into the owner's slot, the owner's own slot is written locally and published by a
+// 128-thread named barrier.  Every CTA is the owner of RO rows, so none exits before the
+// pushes into its shared memory completed.
+static std::string emit_dsmem_splitk_async(const GemmEpilogue& ep, int BN, int CW, int KS, int64_t M, int64_t N,
+                                           const std::string& recv, const std::string& rbar) {
+  std::ostringstream k;
+  const int RO = 128 / KS, PB = BN + 4, TE = BN / 8;
+  k << "  if (warp < 4) {\n  {\n    const int r = warp * 32 + lane, owner = r / " << RO << ";\n";
+  k << "    const unsigned loc = smem_u32(" << recv << ") + (unsigned)((ks * " << RO << " + r % " << RO << ") * " << PB * 4
+    << ");\n";
+  k << "    const unsigned dst = cluster_map(loc, (unsigned)owner), dbar = cluster_map(smem_u32(" << rbar
+    << "), (unsigned)owner);\n";
+  k << "    #pragma unroll 1\n    for (int ch = 0; ch < " << BN / CW << "; ++ch) {\n";
+  k << "      float accr[" << CW << "];\n";
+  k << "      tc_ld" << CW << "(tmem + ((unsigned)(warp * 32) << 16) + (unsigned)(ch * " << CW << "), accr);\n";
+  k << "      if (owner == ks) {\n";
+  k << "        #pragma unroll\n        for (int q = 0; q < " << CW / 4 << "; ++q)\n";
+  k << "          *reinterpret_cast<float4*>(" << recv << " + (ks * " << RO << " + r % " << RO << ") * " << PB * 4
+    << " + (ch * " << CW << " + 4 * q) * 4) = make_float4(accr[4 * q], accr[4 * q + 1], accr[4 * q + 2], accr[4 * q + 3]);\n";
+  k << "      } else {\n";
+  k << "        #pragma unroll\n        for (int q = 0; q < " << CW / 4 << "; ++q)\n";
+  k << "          asm volatile(\"st.async.shared::cluster.mbarrier::complete_tx::bytes.v4.f32 [%0], {%1, %2, %3, %4}, [%5];\"\n"
+       "                       ::\"r\"(dst + (unsigned)((ch * " << CW << " + 4 * q) * 4)), \"f\"(accr[4 * q]), \"f\"(accr[4 * q + 1]),\n"
+       "                       \"f\"(accr[4 * q + 2]), \"f\"(accr[4 * q + 3]), \"r\"(dbar) : \"memory\");\n";
+  k << "      }\n    }\n  }\n";
+  k << "  named_bar_sync(1, 128);\n  mbar_wait(" << rbar << ", 0);\n";
+  k << "  {\n    const float* rcv = reinterpret_cast<const float*>(" << recv << ");\n";
+  k << "    #pragma unroll\n    for (int it = threadIdx.x; it < " << RO * TE << "; it += 128) {\n";
+  k << "      const int rl = it / " << TE << ", tid = it % " << TE << ";\n";
+  k << "      const int gmr = tile_m + ks * " << RO << " + rl;\n";
+  k << "      const int gm = gmr < " << M << " ? gmr : " << M - 1 << ";\n";
+  k << "      const int nb = tile_n;\n";
+  k << "      float acc[8];\n";
+  k << "      #pragma unroll\n      for (int e = 0; e < 8; ++e) acc[e] = 0.f;\n";
+  k << "      #pragma unroll\n      for (int sl = 0; sl < " << KS << "; ++sl) {\n";
+  k << "        const float* src = rcv + (sl * " << RO << " + rl) * " << PB << " + tid * 8;\n";
+  k << "        const float4 a0 = *reinterpret_cast<const float4*>(src), a1 = *reinterpret_cast<const float4*>(src + 4);\n";
+  k << "        acc[0] += a0.x; acc[1] += a0.y; acc[2] += a0.z; acc[3] += a0.w;\n";
+  k << "        acc[4] += a1.x; acc[5] += a1.y; acc[6] += a1.z; acc[7] += a1.w;\n      }\n";
+  k << "      {\n" << ep.body << "      if (gmr < " << M << ") {\n" << ep.store << "      }\n      }\n";
+  k << "    }\n  }\n  }\n";
+  return k.str();
+}
+
 // Column-lane epilogue choice: T = CW / 8 lanes per row unless the output is contiguous
 // along rows (then the row mapping already stores coalesced) or the epilogue reduces rows.
 static int epilogue_lanes(const Graph& g, const Candidate& c, int mm, int CW, const std::vector<Ref>& pre,
@@ -440,8 +489,10 @@ static KernelPlan generate_gather_gemm(const Graph& g, const Candidate& c, int m
     const int S_ = cf.stages ? cf.stages : (int)std::max<int64_t>(2, std::min<int64_t>({NKc, 4, (200 * 1024) / STAGE}));
     if (cf.stages && NKc <= cf.stages) continue;  // identical to the default ring
     const int64_t recv = KS > 1 ? (int64_t)128 * (BN + 4) * 4 : 0;
-    const int64_t REG = std::max<int64_t>((int64_t)S_ * STAGE, recv);
-    const int smem = (int)REG + 1024 + (2 * S_ + 1) * 8 + 16;
+    // split-K receive buffer of its own (barrier-free reduction) when shared memory allows
+    const bool rasync = KS > 1 && (int64_t)S_ * STAGE + recv + 1024 + (2 * S_ + 2) * 8 + 16 <= 227 * 1024;
+    const int64_t REG = rasync ? (int64_t)S_ * STAGE + recv : std::max<int64_t>((int64_t)S_ * STAGE, recv);
+    const int smem = (int)REG + 1024 + (2 * S_ + 2) * 8 + 16;
     const int TE = KS > 1 ? BN / 8 : epilogue_lanes(g, c, mm, 32, pre, (int64_t)S_ * STAGE, &ep);
     const int64_t Nt = (NP + BN - 1) / BN;
     const int tcols = tmem_cols(BN);
@@ -467,7 +518,8 @@ static KernelPlan generate_gather_gemm(const Graph& g, const Candidate& c, int m
     k << "  unsigned long long* full = (unsigned long long*)(smem + " << REG << ");\n";
     k << "  unsigned long long* empty = full + " << S_ << ";\n";
     k << "  unsigned long long* accf = empty + " << S_ << ";\n";
-    k << "  unsigned* tslot = (unsigned*)(accf + 1);\n";
+    if (rasync) k << "  unsigned long long* rbar = accf + 1;\n  unsigned* tslot = (unsigned*)(accf + 2);\n";
+    else k << "  unsigned* tslot = (unsigned*)(accf + 1);\n";
     k << "  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;\n";
     if (KS > 1)
       k << "  const int ks = blockIdx.x % " << KS << ";\n  const int tile_m = (blockIdx.x / " << KS
@@ -478,7 +530,9 @@ static KernelPlan generate_gather_gemm(const Graph& g, const Candidate& c, int m
       << ";\n";
     k << "  if (threadIdx.x == 0) {\n    for (int s = 0; s < " << S_
       << "; ++s) { mbar_init(full + s, 5); mbar_init(empty + s, 1); }\n"
-      << "    mbar_init(accf, 1);\n    mbar_fence_init();\n    tma_prefetch(&tmA);\n";
+      << "    mbar_init(accf, 1);\n" << (rasync ? "    mbar_init(rbar, 1);\n" : "")
+      << "    mbar_fence_init();\n    tma_prefetch(&tmA);\n";
+    if (rasync) k << "    mbar_expect_tx(rbar, " << (int64_t)(KS - 1) * (128 / KS) * BN * 4 << "u);\n";
     // weights (a graph input): first PRE stages fetched before the programmatic-dependency wait
     const bool early = gs.a_src.is_input;
     if (early) {
@@ -490,6 +544,7 @@ static KernelPlan generate_gather_gemm(const Graph& g, const Candidate& c, int m
     k << "  if (warp == 5) tc_alloc(tslot, " << tcols << ");\n";
     k << "  tc_fence_before();\n  __syncthreads();\n  tc_fence_after();\n";
     k << "  const unsigned tmem = *tslot;\n";
+    if (rasync) k << "  asm volatile(\"barrier.cluster.arrive.relaxed.aligned;\\nbarrier.cluster.wait.aligned;\" ::: \"memory\");\n";
     k << "  pdl_trigger();\n  pdl_wait();\n";
     // gather producers: warps 0-3
     k << "  if (warp < 4) {\n";
@@ -565,7 +620,8 @@ static KernelPlan generate_gather_gemm(const Graph& g, const Candidate& c, int m
       k << "  }\n";
     } else {
       k << "  if (warp < 4) {\n    mbar_wait(accf, 0);\n    __syncwarp();\n    tc_fence_after();\n  }\n";
-      k << emit_dsmem_splitk(ep, BN, 32, KS, F, NP, "warp < 4", "warp", 192);
+      if (rasync) k << emit_dsmem_splitk_async(ep, BN, 32, KS, F, NP, "(smem + " + str((int64_t)S_ * STAGE) + ")", "rbar");
+      else k << emit_dsmem_splitk(ep, BN, 32, KS, F, NP, "warp < 4", "warp", 192);
     }
     k << "  tc_fence_before();\n  __syncthreads();\n";
     k << "  if (warp == 5) tc_dealloc(tmem, " << tcols << ");\n}\n";
@@ -588,7 +644,8 @@ static KernelPlan generate_gather_gemm(const Graph& g, const Candidate& c, int m
     kv.smem = smem;
     kv.tma = {da};
     std::ostringstream t;
-    t << gs.tag << " BM=128 BN=" << BN << " BK=64 splitK=" << KS << " stages=" << S_ << (TE > 1 ? " epi=cl" : "");
+    t << gs.tag << " BM=128 BN=" << BN << " BK=64 splitK=" << KS << " stages=" << S_ << (TE > 1 ? " epi=cl" : "")
+      << (rasync ? " red=st.async" : "");
     kv.tag = t.str();
     kp.variants.push_back(kv);
   }
@@ -842,6 +899,172 @@ static KernelPlan generate_prologue_gemm(const Graph& g, const Candidate& c, int
     kp.ext = ep.ext;
     kp.bytes = ep.bytes + pro.bytes + 2 * numel(vb.shape);
     kp.variants.push_back(kv);
+
+    // KB5-PC: cluster-shared prologue.  The variant above recomputes the prologue (e.g. a
+    // LayerNorm over all 128 rows of the A tile) in every CTA of a tile row, serially on 4
+    // warps.  Here a cluster of CN CTAs along N shares the prologue: CTA rank cr TMA-loads
+    // only its RP = 128 / CN rows of the staged input, runs the prologue on them (one or
+    // two rows per warp on up to 16 prologue warps) and TMA-stores the bf16 rows into the
+    // cluster's own copy of A in the kernel's scratch buffer ([Nt / CN][M][K] bf16,
+    // L2-resident; clusters never write the same lines); after a cluster barrier the A
+    // tile comes back from the scratch either multicast (each CTA loads its slice with
+    // .multicast::cluster into all CN CTAs) or per CTA (each CTA loads all 128 rows), so
+    // the prologue runs once per row per cluster.  Single-batch GEMMs only.
+    for (int CNM : {8, 4, -8, -4}) {
+      const int CN = CNM < 0 ? -CNM : CNM;
+      const bool MC = CNM > 0;                   // multicast the slices, else every CTA loads all rows
+      const int RP = 128 / CN;
+      const int PW = RP < 16 ? RP : 16;          // prologue warps (one or two rows each)
+      const int NT = 32 * (PW + 2);              // + the TMA warp PW and the MMA warp PW + 1
+      if (!staged || batch != 1 || !bx_axes.empty() || dx.rank != 2 || Nt % CN || RP % 8) continue;
+      TmaDesc dxs = dx, dsc = dx;
+      dxs.box[1] = (uint32_t)RP;
+      dsc.tensor = -3;
+      dsc.elem_off = 0;
+      dsc.box[1] = (uint32_t)RP;
+      // one scratch copy of the A tile row per cluster (clusters never write the same lines)
+      const int64_t NCL = Nt / CN;
+      dsc.rank = 3;
+      dsc.dims[2] = NCL;
+      dsc.strides[2] = M * K * 2;
+      dsc.box[2] = 1;
+      std::ostringstream q;
+      q << "static __device__ __forceinline__ void tma_load_3d_mc(void* dst, const TmaMap* m, unsigned long long* bar, int c0,\n"
+           "                                                      int c1, unsigned short mask, int c2) {\n"
+           "  asm volatile(\"cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes.multicast::cluster\"\n"
+           "               \" [%0], [%1, {%3, %4, %6}], [%2], %5;\" ::\"r\"(smem_u32(dst)), \"l\"((unsigned long long)m),\n"
+           "               \"r\"(smem_u32(bar)), \"r\"(c0), \"r\"(c1), \"h\"(mask), \"r\"(c2) : \"memory\");\n}\n"
+           "static __device__ __forceinline__ void tma_store_3d(const TmaMap* m, const void* src, int c0, int c1, int c2) {\n"
+           "  asm volatile(\"cp.async.bulk.tensor.3d.global.shared::cta.bulk_group [%0, {%2, %3, %4}], [%1];\" ::\"l\"(\n"
+           "               (unsigned long long)m), \"r\"(smem_u32(src)), \"r\"(c0), \"r\"(c1), \"r\"(c2) : \"memory\");\n}\n";
+      q << "extern \"C\" __global__ void __launch_bounds__(" << NT << ", 1) KNAME(";
+      for (size_t i = 0; i < ep.ext.size(); ++i)
+        q << "const " << (g.dtype_of(ep.ext[i]) == DType::F32 ? "float" : "bf16_t") << "* __restrict__ p" << i << ", ";
+      q << (g.prims[c.output].dtype == DType::F32 ? "float" : "bf16_t") << "* __restrict__ out" << extra_out_params(g, c)
+        << ", bf16_t* __restrict__ scratch, const __grid_constant__ TmaMap tmB, const __grid_constant__ TmaMap tmX, "
+           "const __grid_constant__ TmaMap tmS) {\n";
+      q << "  typedef " << (numel(C) >= (1LL << 31) ? "long long" : "int") << " idx_t;\n  (void)scratch;\n";
+      q << "  extern __shared__ __align__(1024) unsigned char smem_raw[];\n";
+      q << "  unsigned char* smem = (unsigned char*)(((unsigned long long)smem_raw + 1023ull) & ~1023ull);\n";
+      q << "  unsigned long long* full = (unsigned long long*)(smem + " << A_RES + S * B_BYTES << ");\n";
+      q << "  unsigned long long* empty = full + " << S << ";\n";
+      q << "  unsigned long long* afull = empty + " << S << ";\n";
+      q << "  unsigned long long* accf = afull + 1;\n";
+      q << "  unsigned long long* xfull = accf + 1;\n";
+      q << "  unsigned* tslot = (unsigned*)(xfull + 1);\n";
+      q << "  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;\n";
+      q << "  const int tile_n = blockIdx.x * " << BN << ", tile_m = blockIdx.y * 128;\n";
+      q << "  unsigned cr;\n  asm volatile(\"mov.u32 %0, %%cluster_ctarank;\" : \"=r\"(cr));\n";
+      q << "  const int row0 = (int)cr * " << RP << ", cl = (int)(blockIdx.x / " << CN << ");\n";
+      q << "  int bzl = blockIdx.z;\n";
+      for (int b = nbC - 1; b >= 0; --b)
+        q << "  const int " << ep.batch_vars[b] << " = bzl % " << C[b] << "; bzl /= " << C[b] << ";\n";
+      q << "  (void)bzl;\n";
+      std::ostringstream ldxs;
+      ldxs << "    mbar_expect_tx(xfull, " << RP * K * 2 << "u);\n";
+      ldxs << "    for (int kb = 0; kb < " << NKA << "; ++kb)\n";
+      ldxs << "      tma_load_2d(smem + kb * 16384 + row0 * 128, &tmX, xfull, kb * 64, tile_m + row0);\n";
+      q << "  if (threadIdx.x == 0) {\n    for (int s = 0; s < " << S
+        << "; ++s) { mbar_init(full + s, 1); mbar_init(empty + s, 1); }\n"
+        << "    mbar_init(afull, 1);\n    mbar_init(accf, 1);\n    mbar_init(xfull, 1);\n    mbar_fence_init();\n"
+        << "    tma_prefetch(&tmB);\n    tma_prefetch(&tmX);\n    tma_prefetch(&tmS);\n";
+      // armed before the cluster barrier below, so no peer's multicast can precede it
+      q << "    mbar_expect_tx(afull, " << A_RES << "u);\n";
+      if (earlyX) q << ldxs.str();
+      if (PRE) {
+        q << "    for (int s = 0; s < " << PRE << "; ++s) {\n      const int kb = s;\n";
+        q << "      mbar_expect_tx(full + s, " << B_BYTES << "u);\n";
+        q << "      unsigned char* sb = smem + " << A_RES << " + s * " << B_BYTES << ";\n";
+        q << ldb.str() << "    }\n";
+      }
+      q << "  }\n";
+      q << "  if (warp == " << PW + 1 << ") tc_alloc(tslot, " << tcols << ");\n";
+      q << "  tc_fence_before();\n  __syncthreads();\n  tc_fence_after();\n";
+      q << "  const unsigned tmem = *tslot;\n";
+      q << "  asm volatile(\"barrier.cluster.arrive.relaxed.aligned;\\nbarrier.cluster.wait.aligned;\" ::: \"memory\");"
+           "  // every CTA's barriers are initialised and armed\n";
+      q << "  pdl_trigger();\n  pdl_wait();\n";
+      q << "  if (warp < " << PW << ") {\n";
+      if (!earlyX) q << "    if (threadIdx.x == 0) {\n" << ldxs.str() << "    }\n";
+      q << "    const unsigned sA = smem_u32(smem);\n    const int tid = lane;\n    const unsigned gmask = 0xffffffffu;\n"
+        << "    (void)gmask;\n";
+      q << "    mbar_wait(xfull, 0);\n";
+      q << "    #pragma unroll 1\n    for (int r = row0 + warp; r < row0 + " << RP << "; r += " << PW << ") {\n";
+      q << "      const int gm = tile_m + r;\n      if (gm >= " << M << ") break;\n";
+      q << pro.body;
+      q << "    }\n";
+      // the prologue's st.shared -> async proxy; then one thread stores the slice to the
+      // scratch and waits for the bulk writes to complete before the cluster barrier
+      q << "    fence_async_smem();\n    named_bar_sync(1, " << 32 * PW << ");\n";
+      q << "    if (threadIdx.x == 0) {\n";
+      q << "      for (int kb = 0; kb < " << NKA << "; ++kb) tma_store_3d(&tmS, smem + kb * 16384 + row0 * 128, kb * 64, tile_m + row0, cl);\n";
+      q << "      asm volatile(\"cp.async.bulk.commit_group;\" ::: \"memory\");\n";
+      q << "      asm volatile(\"cp.async.bulk.wait_group 0;\" ::: \"memory\");\n";
+      q << "      asm volatile(\"fence.proxy.async.global;\" ::: \"memory\");\n    }\n";
+      q << "    __syncwarp();\n  }\n";
+      q << "  cluster_sync();  // every slice of the A tile is in the scratch\n";
+      q << "  if (warp == " << PW << " && lane == 0) {\n";
+      q << "    asm volatile(\"fence.proxy.async.global;\" ::: \"memory\");\n";
+      if (MC) {
+        q << "    for (int kb = 0; kb < " << NKA << "; ++kb)\n";
+        q << "      tma_load_3d_mc(smem + kb * 16384 + row0 * 128, &tmS, afull, kb * 64, tile_m + row0, (unsigned short)"
+          << ((1 << CN) - 1) << ", cl);\n";
+      } else {
+        q << "    for (int kb = 0; kb < " << NKA << "; ++kb)\n";
+        q << "      for (int c = 0; c < " << CN << "; ++c)\n";
+        q << "        tma_load_3d(smem + kb * 16384 + c * " << RP * 128 << ", &tmS, afull, kb * 64, tile_m + c * " << RP << ", cl);\n";
+      }
+      q << "    int s = 0; unsigned ph = 0;\n";
+      q << "    for (int kb = 0; kb < " << NKA << "; ++kb) {\n";
+      q << "      mbar_wait(empty + s, ph ^ 1u);\n";
+      q << "      if (kb >= " << PRE << ") {\n";
+      q << "      mbar_expect_tx(full + s, " << B_BYTES << "u);\n";
+      q << "      unsigned char* sb = smem + " << A_RES << " + s * " << B_BYTES << ";\n";
+      q << ldb.str() << "      }\n";
+      q << "      if (++s == " << S << ") { s = 0; ph ^= 1u; }\n    }\n";
+      q << "  } else if (warp == " << PW + 1 << " && lane == 0) {\n";
+      q << "    mbar_wait(afull, 0);\n    tc_fence_after();\n";
+      q << "    const unsigned sa0 = smem_u32(smem);\n";
+      q << "    int s = 0; unsigned ph = 0;\n";
+      q << "    for (int kb = 0; kb < " << NKA << "; ++kb) {\n";
+      q << "      mbar_wait(full + s, ph);\n      tc_fence_after();\n";
+      q << "      const unsigned sa = sa0 + kb * 16384, sb = sa0 + " << A_RES << " + s * " << B_BYTES << ";\n";
+      q << "      #pragma unroll\n      for (int k = 0; k < 4; ++k) {\n";
+      q << "        const unsigned long long ad = umma_desc(sa + k * 32, 16, 1024);\n";
+      if (b_kmaj)
+        q << "        const unsigned long long bd = umma_desc(sb + k * 32, 16, 1024);\n";
+      else
+        q << "        const unsigned long long bd = umma_desc(sb + k * " << 16 * b_row_bytes << ", 8192, " << 8 * b_row_bytes
+          << ", " << b_swz_umma << ");\n";
+      q << "        tc_mma(tmem, ad, bd, " << idesc << "u, (kb | k) != 0);\n      }\n";
+      q << "      tc_commit(empty + s);\n";
+      q << "      if (++s == " << S << ") { s = 0; ph ^= 1u; }\n    }\n";
+      q << "    tc_commit(accf);\n  }\n";
+      q << "  __syncwarp();\n";
+      q << "  if (warp < 4) {\n    mbar_wait(accf, 0);\n    __syncwarp();\n    tc_fence_after();\n";
+      q << emit_tmem_epilogue(ep, BN, CW, TE, M, N);
+      q << "  }\n";
+      q << "  tc_fence_before();\n  __syncthreads();\n";
+      q << "  if (warp == " << PW + 1 << ") tc_dealloc(tmem, " << tcols << ");\n}\n";
+      KernelVariant kc;
+      std::string s2 = q.str();
+      std::snprintf(nm, sizeof nm, "korch_pgemm_%016llx", (unsigned long long)fnv1a(std::string(kSm100GemmTemplate) + "\n" + s2));
+      kc.name = nm;
+      s2.replace(s2.find("KNAME"), 5, kc.name);
+      kc.source = s2;
+      kc.tcgen05 = true;
+      kc.block = NT;
+      kc.grid = Nt;
+      kc.grid_y = Mt;
+      kc.grid_z = 1;
+      kc.cluster = CN;
+      kc.smem = smem;
+      kc.scratch_bytes = NCL * M * K * 2;
+      kc.tma = {db, dxs, dsc};
+      kc.tag = t.str() + " cluster-prologue CN=" + std::to_string(CN) + " PW=" + std::to_string(PW) +
+               (MC ? " A=multicast" : " A=per-CTA");
+      kp.variants.push_back(kc);
+    }
   }
   if (!kp.variants.empty()) {
     kp.klass = KORCH_CLASS_GEMM;
@@ -1209,7 +1432,11 @@ KernelPlan generate_gemm(const Graph& g, const Candidate& c) {
     const GemmEpilogue& ep = epv;
     const int RO = 128 / KS, PB = BN + 4;                  // rows owned per CTA, receive pitch (floats)
     const int64_t recv_bytes = KS > 1 ? (int64_t)128 * PB * 4 : 0;
-    const int64_t REG0 = std::max<int64_t>((int64_t)S * STAGE, recv_bytes);
+    // split-K receive buffer: its own region (barrier-free reduction, emit_dsmem_splitk_async)
+    // when shared memory allows, else aliasing the idle operand ring (emit_dsmem_splitk)
+    const bool rasync = KS > 1 && (int64_t)S * STAGE + recv_bytes + side_bytes + 1024 + (2 * S + 3) * 8 + 16 <= 227 * 1024;
+    const int64_t RECV_OFF = rasync ? (int64_t)S * STAGE : 0;
+    const int64_t REG0 = rasync ? (int64_t)S * STAGE + recv_bytes : std::max<int64_t>((int64_t)S * STAGE, recv_bytes);
     const int64_t REG = REG0 + side_bytes;                 // ring (| DSMEM receive) | side tiles
     std::vector<TmaDesc> sdesc;
     std::vector<std::vector<int>> sd_axes;
@@ -1238,8 +1465,8 @@ KernelPlan generate_gemm(const Graph& g, const Candidate& c) {
       sd_axes.push_back(ax);
     }
     if (!side_ok) continue;
-    if (REG + 1024 + (2 * S + 2) * 8 + 16 > 227 * 1024) continue;
-    const int smem = (int)REG + 1024 + (2 * S + 2) * 8 + 16;
+    if (REG + 1024 + (2 * S + 3) * 8 + 16 > 227 * 1024) continue;
+    const int smem = (int)REG + 1024 + (2 * S + 3) * 8 + 16;
     const int tcols = tmem_cols(BN);
     const int64_t Nt = (N + BN - 1) / BN;
     uint32_t idesc = (1u << 4) | (1u << 7) | (1u << 10) | ((a_kmaj ? 0u : 1u) << 15) | ((b_kmaj ? 0u : 1u) << 16) |
@@ -1273,7 +1500,8 @@ KernelPlan generate_gemm(const Graph& g, const Candidate& c) {
     k << "  unsigned long long* empty = full + " << S << ";\n";
     k << "  unsigned long long* accf = empty + " << S << ";\n";
     k << "  unsigned long long* sidef = accf + 1;\n  (void)sidef;\n";
-    k << "  unsigned* tslot = (unsigned*)(accf + 2);\n";
+    if (rasync) k << "  unsigned long long* rbar = accf + 2;\n  unsigned* tslot = (unsigned*)(accf + 3);\n";
+    else k << "  unsigned* tslot = (unsigned*)(accf + 2);\n";
     k << "  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;\n";
     if (KS > 1)  // cluster of KS CTAs along x = the K-slices of one output tile
       k << "  const int ks = blockIdx.x % " << KS << ";\n  const int tile_m = (blockIdx.x / " << KS
@@ -1316,8 +1544,10 @@ KernelPlan generate_gemm(const Graph& g, const Candidate& c) {
     };
     k << "  if (threadIdx.x == 0) {\n    for (int s = 0; s < " << S
       << "; ++s) { mbar_init(full + s, 1); mbar_init(empty + s, 1); }\n"
-      << "    mbar_init(accf, 1);\n    mbar_init(sidef, 1);\n    mbar_fence_init();\n    tma_prefetch(&tmA);\n"
+      << "    mbar_init(accf, 1);\n    mbar_init(sidef, 1);\n" << (rasync ? "    mbar_init(rbar, 1);\n" : "")
+      << "    mbar_fence_init();\n    tma_prefetch(&tmA);\n"
       << "    tma_prefetch(&tmB);\n";
+    if (rasync) k << "    mbar_expect_tx(rbar, " << (int64_t)(KS - 1) * RO * BN * 4 << "u);\n";
     if (!sdesc.empty()) {
       int64_t tot = 0;
       for (auto& d : sdesc) tot += (int64_t)d.box[0] * d.box[1] * (d.dtype ? 2 : 4);
@@ -1338,6 +1568,30 @@ KernelPlan generate_gemm(const Graph& g, const Candidate& c) {
     k << "  if (warp == 2) tc_alloc(tslot, " << tcols << ");\n";
     k << "  tc_fence_before();\n  __syncthreads();\n  tc_fence_after();\n";
     k << "  const unsigned tmem = *tslot;\n";
+    // the receive barriers of every CTA of the cluster are armed before any push
+    // (relaxed arrive: only the mbarrier inits, fenced by fence.mbarrier_init, must be seen)
+    if (rasync) k << "  asm volatile(\"barrier.cluster.arrive.relaxed.aligned;\\nbarrier.cluster.wait.aligned;\" ::: \"memory\");\n";
+    // Graph-input operands the epilogue reads with plain loads after the main loop (bias,
+    // residual; never written inside a plan) are pulled into L2 before the dependency
+    // wait, spread over the grid's threads: in a cold step their first touch is then an
+    // L2 hit instead of an HBM round trip at the end of the critical path.
+    {
+      std::ostringstream pf;
+      for (size_t i = 0; i < ep.ext.size(); ++i) {
+        const Ref& r = ep.ext[i];
+        if (!r.is_input || (r.id == va.src.id && va.src.is_input) || (r.id == vb.src.id && vb.src.is_input)) continue;
+        bool staged = false;
+        for (auto& sd : ep.sides) staged = staged || sd.slot == (int)i;
+        const int64_t lines = (numel(g.shape_of(r)) * dtype_size(g.dtype_of(r)) + 127) / 128;
+        if (staged || lines > (4 << 20) / 128) continue;
+        pf << "    for (unsigned l = pf0; l < " << lines << "u; l += pfn)\n"
+           << "      asm volatile(\"prefetch.global.L2 [%0];\" ::\"l\"((const char*)p" << i << " + (unsigned long long)l * 128));\n";
+      }
+      if (!pf.str().empty())
+        k << "  {\n    const unsigned pfn = gridDim.x * gridDim.y * gridDim.z * blockDim.x;\n"
+          << "    const unsigned pf0 = ((blockIdx.z * gridDim.y + blockIdx.y) * gridDim.x + blockIdx.x) * blockDim.x + threadIdx.x;\n"
+          << pf.str() << "  }\n";
+    }
     k << "  pdl_trigger();\n  pdl_wait();\n";
     // producer
     k << "  if (warp == 0 && lane == 0) {\n";
@@ -1381,7 +1635,8 @@ KernelPlan generate_gemm(const Graph& g, const Candidate& c) {
       }
       k << emit_tmem_epilogue(ep, BN, CW, TE, M, N);
     } else {
-      k << emit_dsmem_splitk(ep, BN, CW, KS, M, N, "true", "warp", 128);
+      if (rasync) k << emit_dsmem_splitk_async(ep, BN, CW, KS, M, N, "(smem + " + str(RECV_OFF) + ")", "rbar");
+      else k << emit_dsmem_splitk(ep, BN, CW, KS, M, N, "true", "warp", 128);
     }
     k << "  tc_fence_before();\n  __syncthreads();\n";
     k << "  if (warp == 2) tc_dealloc(tmem, " << tcols << ");\n}\n";
@@ -1409,7 +1664,7 @@ KernelPlan generate_gemm(const Graph& g, const Candidate& c) {
     std::ostringstream t;
     t << "gemm BM=128 BN=" << BN << " BK=64 splitK=" << KS << " stages=" << S << " A=" << (a_kmaj ? "K" : "M")
       << "-major B=" << (b_kmaj ? "K" : "N") << "-major M=" << M << " N=" << N << " K=" << K << " batch=" << batch
-      << (TE > 1 ? " epi=cl" : "") << (sdesc.empty() ? "" : " side=tma");
+      << (TE > 1 ? " epi=cl" : "") << (sdesc.empty() ? "" : " side=tma") << (rasync ? " red=st.async" : "");
     kv.tag = t.str();
     kp.variants.push_back(kv);
   }

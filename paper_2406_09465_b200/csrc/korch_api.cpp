@@ -463,7 +463,7 @@ static void launch_variant(korch_ctx* ctx, const KernelPlan& plan, int vi, const
   std::vector<CUtensorMap> maps(v.tma.size());
   for (size_t t = 0; t < v.tma.size(); ++t) {
     const TmaDesc& d = v.tma[t];
-    const void* base = d.tensor == -2 ? out : ins.at(d.tensor);
+    const void* base = d.tensor == -2 ? out : d.tensor == -3 ? (const void*)scratch : ins.at(d.tensor);
     encode_tma(d, base, &maps[t]);
     args.push_back(&maps[t]);
   }
@@ -1193,6 +1193,10 @@ korch_status korch_set_orchestration(korch_graph* G, const int64_t* sel, int64_t
           for (auto& w : wr[s2]) for (auto& r : rd[t]) d = d || ov(w, r);
           for (auto& r : rd[s2]) for (auto& w : wr[t]) d = d || ov(r, w);
           for (auto& w : wr[s2]) for (auto& w2 : wr[t]) d = d || ov(w, w2);
+          // two launches of one kernel that owns a scratch buffer (module-wide) never overlap
+          const KernelVariant& va = G->cs[steps[s2].cand].plan.variants[steps[s2].variant];
+          const KernelVariant& vb = G->cs[steps[t].cand].plan.variants[steps[t].variant];
+          d = d || (va.scratch_bytes > 0 && va.name == vb.name);
           if (d) G->deps[t].push_back((int)s2);
         }
     }

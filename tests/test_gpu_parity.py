@@ -287,13 +287,17 @@ def _ln_linear_graph(m, k, n, batch=1):
 
 
 @pytest.mark.gpu
-@pytest.mark.parametrize("m,k,n,batch", [(128, 768, 256, 1), (200, 256, 48, 1), (70, 64, 200, 2)])
+@pytest.mark.parametrize("m,k,n,batch", [(128, 768, 256, 1), (200, 256, 48, 1), (70, 64, 200, 2), (200, 256, 128, 1)])
 def test_prologue_gemm_every_variant(ctx, m, k, n, batch):
     """KB5-P: LayerNorm computed in the GEMM's A prologue (resident swizzled A tile),
-    ragged M and N, batched, every launch variant."""
+    ragged M and N, batched, every launch variant -- including KB5-PC, the cluster-shared
+    prologue (one RP-row slice per CTA, TMA store to the scratch, multicast back), on a
+    full and a ragged (M = 200) tile row."""
     c = Case(ctx, _ln_linear_graph(m, k, n, batch))
     idx = [x["index"] for x in c.cands if "prologue" in _tags(c, x["index"])]
     assert any(len(c.cands[i]["members"]) >= 12 for i in idx)
+    if n in (256, 128):
+        assert any("cluster-prologue CN=8" in _tags(c, i) for i in idx)
     _every_variant(c, idx, exact=False)
 
 
@@ -882,7 +886,7 @@ def _gather_b_graph(m, k, n, b_layout, dtype="bf16"):
 
 @pytest.mark.gpu
 @pytest.mark.parametrize("m,k,n,lay", [(300, 256, 150, "wn"), (128, 64, 19, "wn"), (64, 128, 196, "chw"),
-                                       (96, 64, 676, "chw")])
+                                       (96, 64, 676, "chw"), (256, 1024, 49, "chw")])
 def test_gather_b_gemm_every_variant(ctx, m, k, n, lay):
     """Gather-B GEMM (B gathered into the MN-major SW128 layout by four producer warps;
     8 consecutive columns per 16-byte unaligned read when B is N-contiguous): every
