@@ -1205,7 +1205,7 @@ KernelPlan generate_gemm(const Graph& g, const Candidate& c) {
   //  * split-K (KS > 1) for grids far smaller than the 148 SMs: a cluster of KS CTAs
   //    accumulates the K-slices of one tile in their TMEMs and reduces them through
   //    distributed shared memory (see the KS > 1 epilogue below).
-  struct Cfg { int bn, ks; bool persist = false; };
+  struct Cfg { int bn, ks; bool persist = false; int ew = 1; };
   std::vector<Cfg> cfgs;
   const int64_t NKt = (K + 63) / 64;
   const int64_t Mt = (M + 127) / 128;
@@ -1224,7 +1224,10 @@ KernelPlan generate_gemm(const Graph& g, const Candidate& c) {
     // persistent tile loop with double-buffered TMEM accumulators (large grids only)
     for (int bn : {128, 256}) {
       const int64_t tiles = Mt * ((N + bn - 1) / bn) * batch;
-      if (tiles >= 2 * 148 && bn / 2 < N) cfgs.push_back({bn, 1, true});
+      if (tiles >= 2 * 148 && bn / 2 < N) {
+        cfgs.push_back({bn, 1, true, 1});
+        cfgs.push_back({bn, 1, true, 2});  // two epilogue warps per TMEM lane quarter
+      }
     }
   }
   bool gather_fallback = false;
@@ -1262,7 +1265,9 @@ KernelPlan generate_gemm(const Graph& g, const Candidate& c) {
       const int64_t NK = NKt;
       GemmEpilogue pe = epv;
       const int TE = epilogue_lanes(g, c, mm, CW, pre, 1 << 30, &pe, 0);
-      const int STG = TE > 1 ? stage_bytes(CW) : 0;
+      const int EW = cf.ew, BNh = BN / EW;     // epilogue warp groups, columns each drains
+      if (BNh % CW) continue;
+      const int STG = TE > 1 ? EW * stage_bytes(CW) : 0;
       const int S = (int)std::min<int64_t>(NK < 2 ? 2 : NK, (220 * 1024 - STG - 2048) / STAGE);
       if (S < 2) continue;
       const int64_t STG_OFF = (int64_t)S * STAGE, BAR_OFF = STG_OFF + STG;
@@ -1291,7 +1296,7 @@ KernelPlan generate_gemm(const Graph& g, const Candidate& c) {
         decode << "      const int " << pe.batch_vars[b] << " = bzl % " << C[b] << "; bzl /= " << C[b] << ";\n";
       decode << "      (void)bzl; (void)tile_m; (void)tile_n;\n";
       std::ostringstream k;
-      k << "extern \"C\" __global__ void __launch_bounds__(192, 1) KNAME(";
+      k << "extern \"C\" __global__ void __launch_bounds__(" << 64 + 128 * EW << ", 1) KNAME(";
       for (size_t i = 0; i < kp.ext.size(); ++i)
         k << "const " << (g.dtype_of(kp.ext[i]) == DType::F32 ? "float" : "bf16_t") << "* __restrict__ p" << i << ", ";
       k << (g.prims[c.output].dtype == DType::F32 ? "float" : "bf16_t") << "* __restrict__ out" << extra_out_params(g, c) << ", ";
@@ -1307,7 +1312,7 @@ KernelPlan generate_gemm(const Graph& g, const Candidate& c) {
       k << "  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;\n";
       k << "  if (threadIdx.x == 0) {\n    for (int s = 0; s < " << S
         << "; ++s) { mbar_init(full + s, 1); mbar_init(empty + s, 1); }\n"
-        << "    mbar_init(accfull, 1); mbar_init(accfull + 1, 1); mbar_init(accempty, 128); mbar_init(accempty + 1, 128);\n"
+        << "    mbar_init(accfull, 1); mbar_init(accfull + 1, 1); mbar_init(accempty, " << 128 * EW << "); mbar_init(accempty + 1, " << 128 * EW << ");\n"
         << "    mbar_fence_init();\n    tma_prefetch(&tmA);\n    tma_prefetch(&tmB);\n  }\n";
       k << "  if (warp == 1) tc_alloc(tslot, " << 2 * BN << ");\n";
       k << "  tc_fence_before();\n  __syncthreads();\n  tc_fence_after();\n";
@@ -1357,12 +1362,19 @@ KernelPlan generate_gemm(const Graph& g, const Candidate& c) {
       k << "        if (++s == " << S << ") { s = 0; ph ^= 1u; }\n      }\n";
       k << "      tc_commit(accfull + buf);\n    }\n";
       // epilogue warps 2-5
-      k << "  } else if (warp >= 2) {\n    const int q = warp & 3;\n    int it = 0;\n";
+      k << "  } else if (warp >= 2) {\n    const int q = warp & 3, h = (warp - 2) / 4;\n    (void)h;\n    int it = 0;\n";
       k << "    for (int t = blockIdx.x; t < " << NT << "; t += gridDim.x, ++it) {\n";
       k << "      const int buf = it & 1;\n      const unsigned use = (unsigned)(it >> 1);\n" << decode.str();
       k << "      mbar_wait(accfull + buf, use & 1u);\n      __syncwarp();\n      tc_fence_after();\n";
       k << "      const unsigned tmem_b = tmem + (unsigned)(buf * " << BN << ");\n";
-      k << emit_tmem_epilogue(pe, BN, CW, TE, M, N, "tmem_b", "q", "smem + " + str(STG_OFF));
+      if (EW == 1) {
+        k << emit_tmem_epilogue(pe, BN, CW, TE, M, N, "tmem_b", "q", "smem + " + str(STG_OFF));
+      } else {  // warp group h drains columns [h * BNh, (h + 1) * BNh) of the tile
+        k << "      {\n      const int tile_n_base = tile_n;\n      {\n      const int tile_n = tile_n_base + h * " << BNh << ";\n";
+        k << emit_tmem_epilogue(pe, BNh, CW, TE, M, N, "(tmem_b + (unsigned)(h * " + str(BNh) + "))", "q",
+                                "smem + " + str(STG_OFF) + " + h * " + str(stage_bytes(CW)));
+        k << "      }\n      }\n";
+      }
       k << "      tc_fence_before();\n      mbar_arrive(accempty + buf);\n    }\n  }\n";
       k << "  tc_fence_before();\n  __syncthreads();\n";
       k << "  if (warp == 1) tc_dealloc(tmem, " << 2 * BN << ");\n}\n";
@@ -1375,7 +1387,7 @@ KernelPlan generate_gemm(const Graph& g, const Candidate& c) {
       src.replace(src.find("KNAME"), 5, kv.name);
       kv.source = src;
       kv.tcgen05 = true;
-      kv.block = 192;
+      kv.block = 64 + 128 * EW;
       kv.grid = std::min<int64_t>(NT, 148);
       kv.grid_y = 1;
       kv.grid_z = 1;
@@ -1384,7 +1396,7 @@ KernelPlan generate_gemm(const Graph& g, const Candidate& c) {
       std::ostringstream t;
       t << "gemm-persistent BM=128 BN=" << BN << " BK=64 stages=" << S << " A=" << (a_kmaj ? "K" : "M") << "-major B="
         << (b_kmaj ? "K" : "N") << "-major M=" << M << " N=" << N << " K=" << K << " batch=" << batch
-        << (TE > 1 ? " epi=cl" : "");
+        << (TE > 1 ? " epi=cl" : "") << (EW > 1 ? " epi-warps=8" : "");
       kv.tag = t.str();
       kp.variants.push_back(kv);
       continue;
@@ -1797,108 +1809,121 @@ KernelPlan generate_attention(const Graph& g, const Candidate& c) {
     return s;
   };
   auto load = [&](int rank) { return "tma_load_" + std::to_string(rank) + "d"; };
-  std::ostringstream k;
-  k << "extern \"C\" __global__ void __launch_bounds__(192, 1) KNAME(";
-  for (size_t i = 0; i < kp.ext.size(); ++i)
-    k << "const " << (g.dtype_of(kp.ext[i]) == DType::F32 ? "float" : "bf16_t") << "* __restrict__ p" << i << ", ";
-  k << (g.prims[c.output].dtype == DType::F32 ? "float" : "bf16_t") << "* __restrict__ out" << extra_out_params(g, c) << ", "
-    << "const __grid_constant__ TmaMap tmQ, const __grid_constant__ TmaMap tmK, const __grid_constant__ TmaMap tmV) {\n";
-  k << "  typedef int idx_t;\n";
-  k << "  extern __shared__ __align__(1024) unsigned char smem_raw[];\n";
-  k << "  unsigned char* smem = (unsigned char*)(((unsigned long long)smem_raw + 1023ull) & ~1023ull);\n";
-  k << "  unsigned long long* bars = (unsigned long long*)(smem + " << offB << ");\n";
-  k << "  unsigned long long *ldf = bars, *sfull = bars + 1, *pfull = bars + 2, *ofull = bars + 3, *ldv = bars + 4;\n";
-  k << "  unsigned* tslot = (unsigned*)(bars + 5);\n";
-  k << "  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;\n";
-  k << "  const int tile_m = blockIdx.x * 128;\n";
-  k << "  int bzl = blockIdx.z;\n";
-  for (int b = nb - 1; b >= 0; --b) k << "  const int bz" << b << " = bzl % " << SS[b] << "; bzl /= " << SS[b] << ";\n";
-  k << "  (void)bzl;\n";
-  k << "  if (threadIdx.x == 0) {\n    mbar_init(ldf, 1); mbar_init(sfull, 1); mbar_init(pfull, 4); mbar_init(ofull, 1);\n"
-    << "    mbar_init(ldv, 1);\n"
-    << "    mbar_fence_init();\n    tma_prefetch(&tmQ); tma_prefetch(&tmK); tma_prefetch(&tmV);\n  }\n";
-  k << "  if (warp == 5) tc_alloc(tslot, " << tcols << ");\n";
-  k << "  tc_fence_before();\n  __syncthreads();\n  tc_fence_after();\n";
-  k << "  const unsigned tmem = *tslot;\n";
-  k << "  pdl_trigger();\n  pdl_wait();\n";
-  // TMA: warp 4
-  k << "  if (warp == 4 && lane == 0) {\n";
-  // Q and K on one barrier, V on its own: S = QK^T and the softmax overlap V's arrival
-  k << "    mbar_expect_tx(ldf, " << Q_BYTES + K_BYTES << "u);\n";
-  k << "    mbar_expect_tx(ldv, " << V_BYTES << "u);\n";
-  for (int64_t kb = 0; kb < KB1; ++kb) {
-    k << "    " << load(dq.rank) << "(smem + " << kb * 16384 << ", &tmQ, ldf, " << coords(std::to_string(kb * 64), "tile_m", bq) << ");\n";
-    k << "    " << load(dk.rank) << "(smem + " << offK + kb * N1 * 128 << ", &tmK, ldf, " << coords(std::to_string(kb * 64), "0", bk) << ");\n";
+  // O epilogue: the column-lane mapping (TE2 = 4, staged through shared memory) and, as a
+  // second launch variant, the row mapping (each thread stores its row's 64 contiguous
+  // columns as 16-byte chunks: no staging round trip, L2 merges the row)
+  std::vector<std::pair<GemmEpilogue, int>> ovars{{ep2, TE2}};
+  if (TE2 > 1) {
+    GemmEpilogue e1;
+    std::string e;
+    if (make_gemm_epilogue(g, c, lin[1], 32, ep1.ext, &e1, &e) && e1.ext.size() == ep2.ext.size()) ovars.push_back({e1, 1});
   }
-  if (v_n) {
-    for (int64_t cc = 0; cc < (N2 + 63) / 64; ++cc)
-      k << "    " << load(dv.rank) << "(smem + " << offV + cc * N1 * 128 << ", &tmV, ldv, " << coords(std::to_string(cc * 64), "0", bv) << ");\n";
-  } else {
-    for (int64_t cc = 0; cc < N1 / 64; ++cc)
-      k << "    " << load(dv.rank) << "(smem + " << offV + cc * N2 * 128 << ", &tmV, ldv, " << coords(std::to_string(cc * 64), "0", bv) << ");\n";
-  }
-  // MMA: warp 5
-  k << "  } else if (warp == 5 && lane == 0) {\n";
-  k << "    mbar_wait(ldf, 0);\n    tc_fence_after();\n";
-  k << "    const unsigned sq = smem_u32(smem), sk = sq + " << offK << ", sv = sq + " << offV << ", sp = sq + " << offP << ";\n";
-  k << "    #pragma unroll\n    for (int kb = 0; kb < " << KB1 << "; ++kb)\n";
-  k << "      #pragma unroll\n      for (int k = 0; k < 4; ++k)\n";
-  k << "        tc_mma(tmem, umma_desc(sq + kb * 16384 + k * 32, 16, 1024), umma_desc(sk + kb * " << N1 * 128
-    << " + k * 32, 16, 1024), " << id1 << "u, (kb | k) != 0);\n";
-  k << "    tc_commit(sfull);\n";
-  k << "    mbar_wait(pfull, 0);\n    mbar_wait(ldv, 0);\n    tc_fence_after();\n";
-  k << "    #pragma unroll\n    for (int k0 = 0; k0 < " << N1 << "; k0 += 16) {\n";
-  k << "      const unsigned long long ad = umma_desc(sp + (k0 >> 6) * 16384 + (k0 & 63) * 2, 16, 1024);\n";
-  if (v_n)
-    k << "      const unsigned long long bd = umma_desc(sv + k0 * 128, " << N1 * 128 << ", 1024);\n";
-  else
-    k << "      const unsigned long long bd = umma_desc(sv + (k0 >> 6) * " << N2 * 128 << " + (k0 & 63) * 2, 16, 1024);\n";
-  k << "      tc_mma(tmem + " << N1 << ", ad, bd, " << id2 << "u, k0 != 0);\n    }\n";
-  k << "    tc_commit(ofull);\n  }\n";
-  k << "  __syncwarp();\n";
-  // epilogue warps 0-3: P into smem, then O to HBM
-  k << "  if (warp < 4) {\n";
-  k << "    const int gm = tile_m + warp * 32 + lane;\n    const int tid = 0;\n    (void)tid;\n";
-  k << "    mbar_wait(sfull, 0);\n    __syncwarp();\n    tc_fence_after();\n";
-  k << "    {\n      const int nb = 0;\n      float acc[" << N1 << "];\n";
-  k << "      #pragma unroll\n      for (int q = 0; q < " << N1 / 32 << "; ++q)\n"
-    << "        tc_ld32(tmem + ((unsigned)(warp * 32) << 16) + (unsigned)(q * 32), acc + q * 32);\n";
-  k << ep1.body;
-  k << "      const unsigned sp = smem_u32(smem + " << offP << ");\n";
-  k << "      const int r = warp * 32 + lane;\n";
-  k << "      #pragma unroll\n      for (int q = 0; q < " << N1 / 8 << "; ++q) {\n";
-  k << "        uint4 pk = make_uint4(pack2(" << ep1.store << "[q * 8], " << ep1.store << "[q * 8 + 1]), pack2(" << ep1.store
-    << "[q * 8 + 2], " << ep1.store << "[q * 8 + 3]), pack2(" << ep1.store << "[q * 8 + 4], " << ep1.store << "[q * 8 + 5]), pack2("
-    << ep1.store << "[q * 8 + 6], " << ep1.store << "[q * 8 + 7]));\n";
-  k << "        st_shared_v4(sp + (q >> 3) * 16384 + r * 128 + (((q & 7) ^ (r & 7)) << 4), pk);\n      }\n";
-  k << "    }\n";
-  k << "    fence_async_smem();\n    tc_fence_before();\n    __syncwarp();\n    if (lane == 0) mbar_arrive(pfull);\n";
-  k << "    mbar_wait(ofull, 0);\n    __syncwarp();\n    tc_fence_after();\n";
-  // O epilogue: Q/K/V/P shared memory is idle now (both MMAs done) and serves as the
-  // column-lane staging buffer
-  k << "    const int tile_n = 0;\n    const unsigned tmem_o = tmem + " << N1 << ";\n";
-  k << "  " << emit_tmem_epilogue(ep2, (int)((N2 + 31) / 32 * 32), 32, TE2, M, N2, "tmem_o");
-  k << "  }\n";
-  k << "  tc_fence_before();\n  __syncthreads();\n";
-  k << "  if (warp == 5) tc_dealloc(tmem, " << tcols << ");\n}\n";
-  KernelVariant kv;
-  std::string src = k.str();
   char nm[64];
-  std::snprintf(nm, sizeof nm, "korch_attn_%016llx", (unsigned long long)fnv1a(std::string(kSm100GemmTemplate) + "\n" + src));
-  kv.name = nm;
-  src.replace(src.find("KNAME"), 5, kv.name);
-  kv.source = src;
-  kv.tcgen05 = true;
-  kv.block = 192;
-  kv.grid = (M + 127) / 128;
-  kv.grid_y = 1;
-  kv.grid_z = batch;
-  kv.smem = smem;
-  kv.tma = {dq, dk, dv};
   std::ostringstream t;
   t << "attention BM=128 N1=" << N1 << " K1=" << K1 << " N2=" << N2 << " V=" << (v_n ? "N" : "K") << "-major batch=" << batch;
-  kv.tag = t.str();
-  kp.variants.push_back(kv);
+  for (auto& ov : ovars) {
+    const GemmEpilogue& ep2v = ov.first;
+    const int TE2v = ov.second;
+    std::ostringstream k;
+    k << "extern \"C\" __global__ void __launch_bounds__(192, 1) KNAME(";
+    for (size_t i = 0; i < kp.ext.size(); ++i)
+      k << "const " << (g.dtype_of(kp.ext[i]) == DType::F32 ? "float" : "bf16_t") << "* __restrict__ p" << i << ", ";
+    k << (g.prims[c.output].dtype == DType::F32 ? "float" : "bf16_t") << "* __restrict__ out" << extra_out_params(g, c) << ", "
+      << "const __grid_constant__ TmaMap tmQ, const __grid_constant__ TmaMap tmK, const __grid_constant__ TmaMap tmV) {\n";
+    k << "  typedef int idx_t;\n";
+    k << "  extern __shared__ __align__(1024) unsigned char smem_raw[];\n";
+    k << "  unsigned char* smem = (unsigned char*)(((unsigned long long)smem_raw + 1023ull) & ~1023ull);\n";
+    k << "  unsigned long long* bars = (unsigned long long*)(smem + " << offB << ");\n";
+    k << "  unsigned long long *ldf = bars, *sfull = bars + 1, *pfull = bars + 2, *ofull = bars + 3, *ldv = bars + 4;\n";
+    k << "  unsigned* tslot = (unsigned*)(bars + 5);\n";
+    k << "  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;\n";
+    k << "  const int tile_m = blockIdx.x * 128;\n";
+    k << "  int bzl = blockIdx.z;\n";
+    for (int b = nb - 1; b >= 0; --b) k << "  const int bz" << b << " = bzl % " << SS[b] << "; bzl /= " << SS[b] << ";\n";
+    k << "  (void)bzl;\n";
+    k << "  if (threadIdx.x == 0) {\n    mbar_init(ldf, 1); mbar_init(sfull, 1); mbar_init(pfull, 4); mbar_init(ofull, 1);\n"
+      << "    mbar_init(ldv, 1);\n"
+      << "    mbar_fence_init();\n    tma_prefetch(&tmQ); tma_prefetch(&tmK); tma_prefetch(&tmV);\n  }\n";
+    k << "  if (warp == 5) tc_alloc(tslot, " << tcols << ");\n";
+    k << "  tc_fence_before();\n  __syncthreads();\n  tc_fence_after();\n";
+    k << "  const unsigned tmem = *tslot;\n";
+    k << "  pdl_trigger();\n  pdl_wait();\n";
+    // TMA: warp 4
+    k << "  if (warp == 4 && lane == 0) {\n";
+    // Q and K on one barrier, V on its own: S = QK^T and the softmax overlap V's arrival
+    k << "    mbar_expect_tx(ldf, " << Q_BYTES + K_BYTES << "u);\n";
+    k << "    mbar_expect_tx(ldv, " << V_BYTES << "u);\n";
+    for (int64_t kb = 0; kb < KB1; ++kb) {
+      k << "    " << load(dq.rank) << "(smem + " << kb * 16384 << ", &tmQ, ldf, " << coords(std::to_string(kb * 64), "tile_m", bq) << ");\n";
+      k << "    " << load(dk.rank) << "(smem + " << offK + kb * N1 * 128 << ", &tmK, ldf, " << coords(std::to_string(kb * 64), "0", bk) << ");\n";
+    }
+    if (v_n) {
+      for (int64_t cc = 0; cc < (N2 + 63) / 64; ++cc)
+        k << "    " << load(dv.rank) << "(smem + " << offV + cc * N1 * 128 << ", &tmV, ldv, " << coords(std::to_string(cc * 64), "0", bv) << ");\n";
+    } else {
+      for (int64_t cc = 0; cc < N1 / 64; ++cc)
+        k << "    " << load(dv.rank) << "(smem + " << offV + cc * N2 * 128 << ", &tmV, ldv, " << coords(std::to_string(cc * 64), "0", bv) << ");\n";
+    }
+    // MMA: warp 5
+    k << "  } else if (warp == 5 && lane == 0) {\n";
+    k << "    mbar_wait(ldf, 0);\n    tc_fence_after();\n";
+    k << "    const unsigned sq = smem_u32(smem), sk = sq + " << offK << ", sv = sq + " << offV << ", sp = sq + " << offP << ";\n";
+    k << "    #pragma unroll\n    for (int kb = 0; kb < " << KB1 << "; ++kb)\n";
+    k << "      #pragma unroll\n      for (int k = 0; k < 4; ++k)\n";
+    k << "        tc_mma(tmem, umma_desc(sq + kb * 16384 + k * 32, 16, 1024), umma_desc(sk + kb * " << N1 * 128
+      << " + k * 32, 16, 1024), " << id1 << "u, (kb | k) != 0);\n";
+    k << "    tc_commit(sfull);\n";
+    k << "    mbar_wait(pfull, 0);\n    mbar_wait(ldv, 0);\n    tc_fence_after();\n";
+    k << "    #pragma unroll\n    for (int k0 = 0; k0 < " << N1 << "; k0 += 16) {\n";
+    k << "      const unsigned long long ad = umma_desc(sp + (k0 >> 6) * 16384 + (k0 & 63) * 2, 16, 1024);\n";
+    if (v_n)
+      k << "      const unsigned long long bd = umma_desc(sv + k0 * 128, " << N1 * 128 << ", 1024);\n";
+    else
+      k << "      const unsigned long long bd = umma_desc(sv + (k0 >> 6) * " << N2 * 128 << " + (k0 & 63) * 2, 16, 1024);\n";
+    k << "      tc_mma(tmem + " << N1 << ", ad, bd, " << id2 << "u, k0 != 0);\n    }\n";
+    k << "    tc_commit(ofull);\n  }\n";
+    k << "  __syncwarp();\n";
+    // epilogue warps 0-3: P into smem, then O to HBM
+    k << "  if (warp < 4) {\n";
+    k << "    const int gm = tile_m + warp * 32 + lane;\n    const int tid = 0;\n    (void)tid;\n";
+    k << "    mbar_wait(sfull, 0);\n    __syncwarp();\n    tc_fence_after();\n";
+    k << "    {\n      const int nb = 0;\n      float acc[" << N1 << "];\n";
+    k << "      #pragma unroll\n      for (int q = 0; q < " << N1 / 32 << "; ++q)\n"
+      << "        tc_ld32(tmem + ((unsigned)(warp * 32) << 16) + (unsigned)(q * 32), acc + q * 32);\n";
+    k << ep1.body;
+    k << "      const unsigned sp = smem_u32(smem + " << offP << ");\n";
+    k << "      const int r = warp * 32 + lane;\n";
+    k << "      #pragma unroll\n      for (int q = 0; q < " << N1 / 8 << "; ++q) {\n";
+    k << "        uint4 pk = make_uint4(pack2(" << ep1.store << "[q * 8], " << ep1.store << "[q * 8 + 1]), pack2(" << ep1.store
+      << "[q * 8 + 2], " << ep1.store << "[q * 8 + 3]), pack2(" << ep1.store << "[q * 8 + 4], " << ep1.store << "[q * 8 + 5]), pack2("
+      << ep1.store << "[q * 8 + 6], " << ep1.store << "[q * 8 + 7]));\n";
+    k << "        st_shared_v4(sp + (q >> 3) * 16384 + r * 128 + (((q & 7) ^ (r & 7)) << 4), pk);\n      }\n";
+    k << "    }\n";
+    k << "    fence_async_smem();\n    tc_fence_before();\n    __syncwarp();\n    if (lane == 0) mbar_arrive(pfull);\n";
+    k << "    mbar_wait(ofull, 0);\n    __syncwarp();\n    tc_fence_after();\n";
+    // O epilogue: Q/K/V/P shared memory is idle now (both MMAs done) and serves as the
+    // column-lane staging buffer
+    k << "    const int tile_n = 0;\n    const unsigned tmem_o = tmem + " << N1 << ";\n";
+    k << "  " << emit_tmem_epilogue(ep2v, (int)((N2 + 31) / 32 * 32), 32, TE2v, M, N2, "tmem_o");
+    k << "  }\n";
+    k << "  tc_fence_before();\n  __syncthreads();\n";
+    k << "  if (warp == 5) tc_dealloc(tmem, " << tcols << ");\n}\n";
+    KernelVariant kv;
+    std::string src = k.str();
+    std::snprintf(nm, sizeof nm, "korch_attn_%016llx", (unsigned long long)fnv1a(std::string(kSm100GemmTemplate) + "\n" + src));
+    kv.name = nm;
+    src.replace(src.find("KNAME"), 5, kv.name);
+    kv.source = src;
+    kv.tcgen05 = true;
+    kv.block = 192;
+    kv.grid = (M + 127) / 128;
+    kv.grid_y = 1;
+    kv.grid_z = batch;
+    kv.smem = smem;
+    kv.tma = {dq, dk, dv};
+    kv.tag = t.str() + (TE2v != TE2 ? " O-epi=row" : "");
+    kp.variants.push_back(kv);
+  }
   kp.klass = KORCH_CLASS_GEMM;
   kp.reject.clear();
 

@@ -836,6 +836,11 @@ def _dconv_graph(kind, dtype="bf16"):
         f = b.op("Reshape", f, shape=[1, 12, 16, 24])
         y = b.op("SiLU", b.op("Conv", f, b.input("w", [16, 12, 3, 3], std=0.1), b.input("bias", [16], std=0.1),
                               stride=[1, 1], pads=[1, 1], groups=1))
+    elif kind == "candy_wide":       # reflect pad -> 9x9 conv 32 -> 3, two 128-pixel tiles per row (ragged)
+        x = b.input("x", [1, 32, 6, 200])
+        h = b.op("Pad", x, pads=[[0, 0], [0, 0], [4, 4], [4, 4]], mode="reflect")
+        y = b.op("Conv", h, b.input("w", [3, 32, 9, 9], std=0.02), b.input("bias", [3], std=0.1),
+                 stride=[1, 1], pads=[0, 0], groups=1)
     else:                            # hardswish -> depthwise 3x3 (+bias) -> hardswish
         x = b.input("x", [1, 40, 18, 32])
         y = b.op("HardSwish", b.op("Conv", b.op("HardSwish", x), b.input("w", [40, 1, 3, 3], std=0.3),
@@ -865,6 +870,27 @@ def test_direct_conv_every_variant(ctx, kind, dtype):
             c.check(c.completion([x["index"]]))
             ran += 1
     assert ran >= 2
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("kind", ["candy_out", "candy_in", "focus", "candy_wide"])
+def test_tc_direct_conv_every_variant(ctx, kind):
+    """KB6-D tensor-core direct convolution (descriptor-offset implicit GEMM over the staged
+    input window): every candidate carrying it, inside a feasible orchestration, matches
+    the oracle -- reflect / zero padding, Focus views, channel padding to 16, filters
+    padded to N = 16 / 32, ragged 128-pixel row tiles."""
+    c = Case(ctx, _dconv_graph(kind))
+    ran = 0
+    for x in c.cands:
+        if x["klass"] == "rejected":
+            continue
+        for v, nm in enumerate(c.kg.variant_names(x["index"])):
+            if not nm.startswith("korch_tconv"):
+                continue
+            c.kg.set_variant(x["index"], v)
+            c.check(c.completion([x["index"]]))
+            ran += 1
+    assert ran >= 1
 
 
 def _gather_b_graph(m, k, n, b_layout, dtype="bf16"):
