@@ -18,6 +18,7 @@ def main():
     ap.add_argument("--max-members", type=int, default=2)
     ap.add_argument("--limit", type=int, default=8)
     ap.add_argument("--prefix", default="korch_dconv")
+    ap.add_argument("--cands", default="", help="comma list of candidate indices (instead of the first --limit)")
     a = ap.parse_args()
     import paper_2406_09465_b200 as K
     from bench import model_enum_opts, model_graph
@@ -27,6 +28,8 @@ def main():
     kinds = {n["id"]: n["kind"] for n in kg.prim["nodes"]}
     ids = [c["index"] for c in cs if c["klass"] != "rejected" and len(c["members"]) <= a.max_members
            and any(n.startswith(a.prefix) for n in kg.variant_names(c["index"]))][: a.limit]
+    if a.cands:
+        ids = [int(x) for x in a.cands.split(",")]
     kg.profile(ids)
     for i in ids:
         src = kg.source(i)

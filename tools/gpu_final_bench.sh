@@ -9,6 +9,7 @@ timeout ${BENCH_TIMEOUT:-1500} python bench.py --save-selection gpurun_out/sel_c
 echo "bench rc $?" >> gpurun_out/bench.err
 if [ -z "$SKIP_N2" ]; then
   KORCH_DIST_BACKEND=gloo timeout 900 python bench.py --gpus 2 --steps 10 --warmup 3 --no-cpu-baseline --no-bw-variant \
+    --models candy,efficientvit --scaling-models candy \
     > gpurun_out/bench_n2.log 2>gpurun_out/bench_n2.err; echo "bench n2 rc $?" >> gpurun_out/bench_n2.err
 fi
 export KORCH_EXEC_DIRECT=1
