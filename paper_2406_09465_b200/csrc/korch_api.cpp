@@ -878,9 +878,10 @@ korch_status korch_profile(korch_graph* G, const int64_t* idx, int64_t n, const 
           continue;
         }
       }
-      // scratch buffers at the candidate's exact shapes
+      // scratch buffers at the candidate's exact shapes (512 bytes of slack before the
+      // first and after the last: a kernel's speculated boundary load stays mapped)
       std::vector<size_t> offs;
-      size_t tot = 0;
+      size_t tot = 512;
       for (auto& r : s.plan.ext) {
         offs.push_back(tot);
         tot += ((size_t)tensor_bytes(G->g, r) + 255) & ~(size_t)255;
@@ -894,7 +895,7 @@ korch_status korch_profile(korch_graph* G, const int64_t* idx, int64_t n, const 
           tot += ((size_t)tensor_bytes(G->g, Ref{false, o}) + 255) & ~(size_t)255;
         }
       }
-      CUdeviceptr base = ctx->arena_get(tot);
+      CUdeviceptr base = ctx->arena_get(tot + 512);
       std::vector<const void*> ins;
       for (size_t e = 0; e < s.plan.ext.size(); ++e) {
         const Ref& r = s.plan.ext[e];
