@@ -30,6 +30,9 @@ PATTERNS = {
     "STG.128": r"\bSTG\.E\.\S*128|\bSTG\.E\.128\b",
     "SHFL": r"\bSHFL\b",
     "ACQBULK/UBLKCP (bulk copy)": r"\bUBLKCP\b",
+    "UTMALDG multicast": r"\bUTMALDG\S*MULTICAST",
+    "STAS (st.async, DSMEM + mbarrier)": r"\bSTAS\b",
+    "UCGABAR (cluster barrier)": r"\bUCGABAR_\w+",
 }
 
 
