@@ -16,6 +16,7 @@ from __future__ import annotations
 
 import argparse
 import json
+import math
 import os
 import statistics
 import subprocess
@@ -231,14 +232,39 @@ def dist_summary(ts):
 FP32_SIMT_TFLOPS = 148 * 128 * 2 * 1.965e9 / 1e12
 
 
+def linear_flops(kg, members):
+    """2 x multiply-adds of the dense linear members (Conv2d, MatMul) of a candidate, from the
+    primitive graph's shapes: the flops of a window / contraction kernel whose template did
+    not record them (a row-template plan carrying a direct-convolution variant)."""
+    nodes = {n["id"]: n for n in kg.prim["nodes"]}
+    ins = {x["name"]: x["shape"] for x in kg.prim["inputs"]}
+
+    def shape(ref):
+        return ins[ref["input"]] if "input" in ref else nodes[ref["node"]]["shape"]
+    f = 0.0
+    for m in members:
+        n = nodes[m]
+        if n["kind"] == "conv2d":
+            w = shape(n["inputs"][1])                     # [F, C / groups, R, S]
+            f += 2.0 * math.prod(n["shape"]) * w[1] * w[2] * w[3]
+        elif n["kind"] == "matmul":
+            a = shape(n["inputs"][0])
+            f += 2.0 * math.prod(n["shape"]) * a[-1]
+    return f
+
+
 def roofline_of(kg, cands, i, cold_ns, pk):
     """Roofline of candidate i from its algorithmic bytes / flops and a cold-L2 time:
-    tcgen05 kernels against the bf16 tensor peak or HBM, SIMT kernels with flops
-    (direct conv, skinny-K MatMul) against the FP32 FMA peak ("alu") or HBM."""
-    c = cands[i]
+    tcgen05 kernels (GEMMs, attention, the KB6-D tensor-core direct convolution) against
+    the bf16 tensor peak or HBM, SIMT kernels with flops (direct conv, skinny-K MatMul)
+    against the FP32 FMA peak ("alu") or HBM."""
+    c = dict(cands[i])
     name = kg.kernel_name(i)
-    simt = not (name.startswith("korch_gemm") or name.startswith("korch_pgemm") or name.startswith("korch_conv")
-                or name.startswith("korch_gg") or name.startswith("korch_attn"))
+    if c["flops"] <= 0:
+        c["flops"] = linear_flops(kg, c["members"])
+    tensor = (name.startswith("korch_gemm") or name.startswith("korch_pgemm") or name.startswith("korch_conv")
+              or name.startswith("korch_gg") or name.startswith("korch_attn") or name.startswith("korch_tconv"))
+    simt = not tensor
     if simt and c["flops"] > 0 and c["flops"] / (FP32_SIMT_TFLOPS * 1e12) > c["bytes"] / (pk["hbm_gbs"] * 1e9):
         ach = c["flops"] / (cold_ns * 1e-9) / 1e12
         r = {"bound": "alu", "achieved": ach, "peak": FP32_SIMT_TFLOPS, "unit": "TFLOP/s",
@@ -249,7 +275,7 @@ def roofline_of(kg, cands, i, cold_ns, pk):
                   "variant": kg.variant_info(i)[2]})
         return r
     ridge = pk["bf16_tflops"] * 1e12 / (pk["hbm_gbs"] * 1e9)
-    ai = c["flops"] / max(1, c["bytes"]) if c["klass"] == "gemm" and not simt else 0.0
+    ai = c["flops"] / max(1, c["bytes"]) if tensor else 0.0
     if ai > ridge:
         ach = c["flops"] / (cold_ns * 1e-9) / 1e12
         r = {"bound": "tensor", "achieved": ach, "peak": pk["bf16_tflops"], "unit": "TFLOP/s"}
